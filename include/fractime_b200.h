@@ -1,0 +1,150 @@
+/*
+ * fractime_b200.h -- C ABI of the B200-native fast solver for the block
+ * lower-triangular Toeplitz (BLTT) systems of the L1 Caputo schemes
+ * (arXiv 1710.11593).  Drop-in for the reference `fractime` solver entry
+ * points (scheme setup, direct solve, fast solve); see INTEGRATION.md for the
+ * ctypes / C++ bindings a maintainer adds on the reference side.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   ft_setup / ft_setup_batch  <- validate()                       src/schemes.cpp:58-78
+ *                                 SchemeConstants::for_spec()       src/schemes.cpp:44-56
+ *                                 g_weights()/m_weights()           src/weights.cpp:28-40
+ *                                 assemble_scheme4() (column)       src/schemes.cpp:381-399
+ *                                 assemble_scheme3_reordered()      src/schemes.cpp:272-288
+ *                                 embed_circulant() (spectra)       src/toeplitz.cpp:84-96
+ *   ft_column                  <- ToeplitzOperator::first_col()     include/fractime/toeplitz.hpp:38
+ *   ft_assemble_rhs            <- assemble_scheme4() rhs            src/schemes.cpp:401-408
+ *                                 Scheme3Rhs::operator()            src/schemes.cpp:300-306
+ *   ft_solve_direct            <- solve(spec, SolveMethod::Direct)  src/schemes.cpp:434-463, :333-352
+ *                                 lower_toeplitz_forward_solve()    src/toeplitz.cpp:169-186
+ *   ft_solve_fast              <- solve(spec, SolveMethod::Fast)    src/schemes.cpp:464-474, :353-369
+ *                                 (GMRES + FFT matvec, src/krylov.cpp:107-223, replaced by a
+ *                                 time-axis divide-and-conquer; same system, same answer)
+ *   ft_last_error              <- the what() of the reference's std::exception
+ *
+ * Conventions
+ *   - Layout: node-major, values[(i-1)*N + (n-1)] = U_i^n, i = 1..cells-1,
+ *     n = 1..N (reference include/fractime/schemes.hpp:209-223).  Batched
+ *     plans stack problems: problem b starts at b*(cells-1)*N.  The ODE has
+ *     one "node".
+ *   - Pointers passed to ft_assemble_rhs_grid / ft_solve_* may be host or
+ *     device memory (detected per call).  Host buffers are staged through
+ *     plan-owned device memory; device buffers are used in place.  rhs == u
+ *     is allowed (in-place solve).
+ *   - Errors: functions return FT_OK (0) or a negative FT_E* code; the
+ *     message (reference wording where one exists) is in ft_last_error(),
+ *     thread-local.  There is no CPU fallback: without a usable CUDA device
+ *     every compute entry point fails with FT_ECUDA.
+ *   - Threading: a plan is immutable after setup apart from its staging
+ *     buffers; use one plan per host thread (distinct plans may run
+ *     concurrently on distinct streams).
+ */
+#ifndef FRACTIME_B200_H
+#define FRACTIME_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Scheme ids follow the reference enum SchemeId (schemes.hpp:182):
+ * Ode2Sided=0 (here: the one-sided fractional ODE of BASELINE config 1, built
+ * from the reference Toeplitz API as in SURVEY.md 3.4), Hyperbolic=1 (not
+ * provided), DiffusionWave=2 (reference Scheme 3), Diffusion=3 (Scheme 4). */
+enum {
+    FT_SCHEME_ODE = 0,
+    FT_SCHEME_WAVE = 2,
+    FT_SCHEME_DIFFUSION = 3
+};
+
+enum {
+    FT_OK = 0,
+    FT_EINVAL = -1,   /* std::invalid_argument */
+    FT_EDOM = -2,     /* std::domain_error     */
+    FT_ELENGTH = -3,  /* std::length_error     */
+    FT_ESOLVER = -4,  /* std::runtime_error    */
+    FT_ECUDA = -5,
+    FT_ENOMEM = -6
+};
+
+/* Right-hand-side mode for the wave scheme (Scheme 3): the reference omits
+ * the c*M_0*u0 term in the n = 1 row (schemes.cpp:304).  Mode 0 reproduces
+ * the reference; mode 1 adds the term. */
+enum { FT_RHS_REFERENCE = 0, FT_RHS_CORRECTED_N1 = 1 };
+
+typedef struct ft_problem {
+    int scheme;            /* FT_SCHEME_* */
+    double gamma;          /* Caputo order: (0,1) ODE/diffusion, (1,2) wave */
+    uint64_t time_steps;   /* N, tau = time_length / N */
+    uint64_t space_cells;  /* reference M (cells); interior nodes = cells-1; ignored for ODE */
+    double time_length;    /* T */
+    double space_length;   /* L, h = L / cells */
+} ft_problem;
+
+typedef struct ft_options {
+    int rhs_mode;          /* FT_RHS_*; wave scheme only */
+    int near_field;        /* lags < near_field are summed exactly in every history
+                              product (0 = default: 1 for ODE/diffusion, 64 for wave) */
+    int device;            /* CUDA device ordinal (-1 = current) */
+    int reserved;
+} ft_options;
+
+typedef struct ft_report {
+    char method[16];       /* "fast" / "direct" (SolveReport::method) */
+    uint64_t iterations;   /* 0: both paths are direct methods (no Krylov matvecs) */
+    double residual;       /* 0 (as for the reference's direct path) */
+    double seconds;        /* wall time of the call (SolveReport::seconds) */
+    double device_ms;      /* device time of the solve proper (CUDA events) */
+    uint64_t kernel_launches;  /* kernels this library launched for the call */
+} ft_report;
+
+typedef struct ft_plan_info {
+    uint64_t problems;     /* batch size B */
+    uint64_t nodes;        /* interior nodes per problem (1 for the ODE) */
+    uint64_t time_steps;   /* N */
+    uint64_t leaf;         /* D&C leaf length */
+    uint64_t levels;       /* history-product levels */
+    uint64_t slabs;        /* spatial slabs (CTAs) per problem in the leaf solve */
+    double h, tau;
+    double mu, c;          /* SchemeConstants of problem 0 */
+} ft_plan_info;
+
+typedef struct ft_plan ft_plan;
+
+/* forcing(x, t, user) and initial data u0(x, user) / phi(x, user), evaluated
+ * at the reference's points: diffusion/ODE (i h, n tau); wave (i h, (n-1/2) tau). */
+typedef double (*ft_forcing_fn)(double x, double t, void* user);
+typedef double (*ft_initial_fn)(double x, void* user);
+
+int ft_setup(const ft_problem* problem, const ft_options* options, ft_plan** out);
+int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options* options,
+                   ft_plan** out);
+int ft_plan_get_info(const ft_plan* plan, ft_plan_info* info);
+int ft_column(const ft_plan* plan, uint64_t problem, double* col_host);
+
+int ft_assemble_rhs(const ft_plan* plan, ft_forcing_fn forcing, ft_initial_fn u0,
+                    ft_initial_fn phi, void* user, double* rhs_host);
+/* Same, from the forcing already sampled at the scheme's points (node-major
+ * grid F) and initial data arrays (nodes per problem, NULL = 0). */
+int ft_assemble_rhs_grid(const ft_plan* plan, const double* forcing_grid, const double* u0,
+                         const double* phi, double* rhs);
+/* Device generation of a separable forcing
+ *   f_b(x, t) = sum_j a[b*nmodes+j] * trig_j(k_j pi x) * t^{p[b*nmodes+j]}
+ * (trig 0 = sin, 1 = cos, 2 = 1), u0_b(x) = u0_amp[b] sin(pi x), phi likewise. */
+int ft_assemble_rhs_modes(const ft_plan* plan, int nmodes, const double* a, const double* k,
+                          const double* p, const int* trig, const double* u0_amp,
+                          const double* phi_amp, double* rhs_device);
+
+int ft_solve_fast(ft_plan* plan, const double* rhs, double* u, ft_report* report);
+int ft_solve_direct(ft_plan* plan, const double* rhs, double* u, ft_report* report);
+
+int ft_set_stream(ft_plan* plan, void* cuda_stream);
+const char* ft_last_error(void);
+void ft_destroy(ft_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRACTIME_B200_H */

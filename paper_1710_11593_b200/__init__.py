@@ -1,0 +1,316 @@
+"""fractime-b200: B200-native fast solver for the L1-Caputo BLTT systems.
+
+Python host mirror of the reference's solver interface (reference
+include/fractime/schemes.hpp): ``ProblemSpec``, ``SchemeId``, ``SolveMethod``,
+``solve(spec, method)`` returning a ``SchemeSolution`` with a ``SolutionGrid``
+and a ``SolveReport``.  Everything is a thin ctypes layer over the C ABI of
+``libfractime_b200.so`` (include/fractime_b200.h); all arithmetic runs in the
+CUDA kernels of that library.  There is no CPU path: if the library or a CUDA
+device is missing, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libfractime_b200.so"
+
+
+class FractimeError(RuntimeError):
+    """Raised for FT_E* codes; .code holds the C ABI code."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(FractimeError, ValueError):
+    pass
+
+
+class DomainError(FractimeError, ValueError):
+    pass
+
+
+class SchemeId(enum.IntEnum):  # reference schemes.hpp:182 (Hyperbolic not provided)
+    Ode = 0
+    DiffusionWave = 2
+    Diffusion = 3
+
+
+class SolveMethod(enum.Enum):  # reference schemes.hpp:184 (Dense/Cg are Scheme 1 only)
+    Direct = "direct"
+    Fast = "fast"
+
+
+FT_RHS_REFERENCE = 0
+FT_RHS_CORRECTED_N1 = 1
+
+
+class _Problem(C.Structure):
+    _fields_ = [("scheme", C.c_int), ("gamma", C.c_double), ("time_steps", C.c_uint64),
+                ("space_cells", C.c_uint64), ("time_length", C.c_double),
+                ("space_length", C.c_double)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("rhs_mode", C.c_int), ("near_field", C.c_int), ("device", C.c_int),
+                ("reserved", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("method", C.c_char * 16), ("iterations", C.c_uint64), ("residual", C.c_double),
+                ("seconds", C.c_double), ("device_ms", C.c_double),
+                ("kernel_launches", C.c_uint64)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("problems", C.c_uint64), ("nodes", C.c_uint64), ("time_steps", C.c_uint64),
+                ("leaf", C.c_uint64), ("levels", C.c_uint64), ("slabs", C.c_uint64),
+                ("h", C.c_double), ("tau", C.c_double), ("mu", C.c_double), ("c", C.c_double)]
+
+
+FORCING_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_double, C.c_void_p)
+INITIAL_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+
+_lib = None
+
+ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
+               "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
+               "ft_set_stream", "ft_last_error", "ft_destroy")
+
+
+def lib() -> C.CDLL:
+    """Load libfractime_b200.so (build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FractimeError(-5, f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        P, D, U64, I = C.c_void_p, C.POINTER(C.c_double), C.c_uint64, C.c_int
+        L.ft_setup.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(P)]
+        L.ft_setup_batch.argtypes = [C.POINTER(_Problem), U64, C.POINTER(_Options), C.POINTER(P)]
+        L.ft_plan_get_info.argtypes = [P, C.POINTER(_Info)]
+        L.ft_column.argtypes = [P, U64, P]
+        L.ft_assemble_rhs.argtypes = [P, FORCING_FN, INITIAL_FN, INITIAL_FN, P, P]
+        L.ft_assemble_rhs_grid.argtypes = [P, P, P, P, P]
+        L.ft_assemble_rhs_modes.argtypes = [P, I, P, P, P, P, P, P, P]
+        L.ft_solve_fast.argtypes = [P, P, P, C.POINTER(_Report)]
+        L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
+        L.ft_set_stream.argtypes = [P, P]
+        L.ft_last_error.restype = C.c_char_p
+        L.ft_destroy.argtypes = [P]
+        L.ft_destroy.restype = None
+        for name in ABI_SYMBOLS:
+            if name not in ("ft_last_error", "ft_destroy"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().ft_last_error().decode()
+        if rc == -1:
+            raise InvalidArgument(rc, msg)
+        if rc == -2:
+            raise DomainError(rc, msg)
+        raise FractimeError(rc, msg)
+
+
+def _ptr(a) -> int:
+    """Device pointer of a torch tensor or host pointer of a numpy array."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous()
+        return a.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+@dataclass
+class ProblemSpec:
+    """Reference ProblemSpec (schemes.hpp:191-205).  Callbacks take (x, t) / (x)."""
+
+    scheme: SchemeId = SchemeId.Diffusion
+    gamma: float = 0.5
+    time_steps: int = 2
+    space_cells: int = 0
+    time_length: float = 1.0
+    space_length: float = 1.0
+    forcing: Optional[Callable[[float, float], float]] = None
+    initial_u0: Optional[Callable[[float], float]] = None
+    initial_phi: Optional[Callable[[float], float]] = None
+    exact: Optional[Callable[[float, float], float]] = None
+
+    def tau(self) -> float:
+        return self.time_length / self.time_steps
+
+    def h(self) -> float:
+        return self.space_length / self.space_cells if self.space_cells else 0.0
+
+    def _c(self) -> _Problem:
+        return _Problem(int(self.scheme), float(self.gamma), int(self.time_steps),
+                        int(self.space_cells), float(self.time_length), float(self.space_length))
+
+
+@dataclass
+class SolutionGrid:
+    """Reference SolutionGrid (schemes.hpp:213-223): node-major values."""
+
+    scheme: SchemeId
+    tau: float
+    h: float
+    time_steps: int
+    space_cells: int
+    values: np.ndarray
+
+    def at(self, i: int, n: int) -> float:
+        return float(self.values[(i - 1) * self.time_steps + (n - 1)])
+
+
+@dataclass
+class SolveReport:
+    method: str = ""
+    iterations: int = 0
+    residual: float = 0.0
+    seconds: float = 0.0
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+@dataclass
+class SchemeSolution:
+    grid: SolutionGrid
+    report: SolveReport = field(default_factory=SolveReport)
+
+
+class Plan:
+    """A device-resident solver plan (ft_setup / ft_setup_batch)."""
+
+    def __init__(self, problems, rhs_mode: int = FT_RHS_REFERENCE, near_field: int = 0,
+                 device: int = -1):
+        if isinstance(problems, ProblemSpec):
+            problems = [problems]
+        self.specs = list(problems)
+        arr = (_Problem * len(self.specs))(*[p._c() for p in self.specs])
+        opt = _Options(rhs_mode, near_field, device, 0)
+        h = C.c_void_p()
+        _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))
+        self._h = h
+        info = _Info()
+        _check(lib().ft_plan_get_info(self._h, C.byref(info)))
+        self.info = info
+        self.B = int(info.problems)
+        self.nodes = int(info.nodes)
+        self.N = int(info.time_steps)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.ft_destroy(h)
+            self._h = None
+
+    @property
+    def shape(self):
+        return (self.B * self.nodes, self.N)
+
+    def column(self, problem: int = 0) -> np.ndarray:
+        out = np.empty(self.N)
+        _check(lib().ft_column(self._h, problem, out.ctypes.data))
+        return out
+
+    def assemble_rhs(self, forcing, u0=None, phi=None) -> np.ndarray:
+        """Host callbacks, evaluated at the reference's points (slow; small sizes)."""
+        f = FORCING_FN(lambda x, t, _u: forcing(x, t))
+        g = INITIAL_FN(lambda x, _u: u0(x)) if u0 else C.cast(None, INITIAL_FN)
+        q = INITIAL_FN(lambda x, _u: phi(x)) if phi else C.cast(None, INITIAL_FN)
+        out = np.empty(self.shape)
+        _check(lib().ft_assemble_rhs(self._h, f, g, q, None, out.ctypes.data))
+        return out
+
+    def assemble_rhs_grid(self, F: np.ndarray, u0=None, phi=None) -> np.ndarray:
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        u0 = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
+        phi = None if phi is None else np.ascontiguousarray(phi, dtype=np.float64)
+        out = np.empty(self.shape)
+        _check(lib().ft_assemble_rhs_grid(self._h, _ptr(F), _ptr(u0), _ptr(phi), out.ctypes.data))
+        return out
+
+    def assemble_rhs_modes(self, out, a, k, p, trig, u0amp=None, phiamp=None):
+        """Device generation of a separable forcing into the device buffer `out`."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        trig = np.ascontiguousarray(trig, dtype=np.int32)
+        u0amp = None if u0amp is None else np.ascontiguousarray(u0amp, dtype=np.float64)
+        phiamp = None if phiamp is None else np.ascontiguousarray(phiamp, dtype=np.float64)
+        _check(lib().ft_assemble_rhs_modes(self._h, len(k), a.ctypes.data, k.ctypes.data,
+                                           p.ctypes.data, trig.ctypes.data,
+                                           None if u0amp is None else u0amp.ctypes.data,
+                                           None if phiamp is None else phiamp.ctypes.data, _ptr(out)))
+        return out
+
+    def _solve(self, fn, rhs, out):
+        if out is None:
+            out = np.empty(self.shape) if isinstance(rhs, np.ndarray) else rhs.new_empty(self.shape)
+        rep = _Report()
+        _check(fn(self._h, _ptr(rhs), _ptr(out), C.byref(rep)))
+        report = SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
+                             rep.device_ms, rep.kernel_launches)
+        return out, report
+
+    def solve_fast(self, rhs, out=None):
+        return self._solve(lib().ft_solve_fast, rhs, out)
+
+    def solve_direct(self, rhs, out=None):
+        return self._solve(lib().ft_solve_direct, rhs, out)
+
+
+def solve(spec: ProblemSpec, method: SolveMethod = SolveMethod.Fast, rhs_mode: int = 0) -> SchemeSolution:
+    """Reference solve(spec, method, cfg) (schemes.cpp:481-489) on the GPU."""
+    t0 = time.perf_counter()
+    plan = Plan(spec, rhs_mode=rhs_mode)
+    rhs = plan.assemble_rhs(spec.forcing, spec.initial_u0, spec.initial_phi)
+    if method == SolveMethod.Fast:
+        u, rep = plan.solve_fast(rhs)
+    else:
+        u, rep = plan.solve_direct(rhs)
+    rep.seconds = time.perf_counter() - t0
+    grid = SolutionGrid(spec.scheme, spec.tau(), spec.h(), spec.time_steps, spec.space_cells,
+                        u.reshape(-1))
+    return SchemeSolution(grid, rep)
+
+
+def l2_error(grid: SolutionGrid, spec: ProblemSpec) -> float:
+    """Reference l2_error (schemes.cpp:525-542); the ODE variant uses the one-sided
+    scheme's nodes n = 1..N."""
+    if spec.exact is None:
+        raise InvalidArgument(-1, "l2_error: spec has no exact solution")
+    acc = 0.0
+    if grid.scheme == SchemeId.Ode:
+        for n in range(1, grid.time_steps + 1):
+            e = grid.values[n - 1] - spec.exact(0.0, n * grid.tau)
+            acc += grid.tau * e * e
+    else:
+        tf = grid.time_steps * grid.tau
+        for i in range(1, grid.space_cells):
+            e = grid.at(i, grid.time_steps) - spec.exact(i * grid.h, tf)
+            acc += grid.h * e * e
+    return math.sqrt(acc)
+
+
+__all__ = ["FractimeError", "InvalidArgument", "DomainError", "SchemeId", "SolveMethod", "ProblemSpec",
+           "SolutionGrid", "SolveReport", "SchemeSolution", "Plan", "solve", "l2_error", "lib",
+           "ABI_SYMBOLS", "FT_RHS_REFERENCE", "FT_RHS_CORRECTED_N1"]

@@ -1,0 +1,686 @@
+// api.cu -- C ABI (include/fractime_b200.h): scheme setup on the host
+// (bit-identical to the reference: same libm calls, same expression order,
+// no FMA contraction in host code), device-resident plan, and the
+// divide-and-conquer driver.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fractime_b200.h"
+#include "internal.cuh"
+
+using namespace ftb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define FT_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return set_err(FT_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                         " at " #call);                                      \
+    } while (0)
+
+struct Level {
+    int n, m, K, G, groups;
+    uint64_t spec_off;  // in cplx, per level block [B][K][m]
+};
+
+enum OpKind { OP_LEAF, OP_MP };
+struct Op {
+    OpKind kind;
+    uint64_t t0;   // leaf: first step; mp: lo
+    int len;       // leaf steps
+    int level;     // mp level index
+    uint64_t mid, hi;
+    bool first;    // reads R from the caller's rhs (first touch)
+};
+
+}  // namespace
+
+struct ft_plan {
+    int scheme = 0;
+    int B = 1;
+    uint64_t N = 0;
+    uint64_t cells = 0;
+    int nodes = 1;
+    double h = 0, tau = 0;
+    int rhs_mode = 0;
+    int J = 1;
+    int device = 0;
+    std::vector<double> gamma;
+    std::vector<double> mu, c;
+    std::vector<double> col_h;   // [B][N]
+    std::vector<double> wts_h;   // [B][N+1] G or M weights
+    std::vector<ProblemConst> pc_h;
+    // leaf configuration
+    int kind = SK_DIAG;
+    int L = 32, npt = 1, threads = 32, slab = 1, P = 1;
+    bool multi = false;
+    // levels
+    std::vector<Level> levels;
+    std::vector<Op> ops;
+    int logT = 4;
+    // device state
+    ProblemConst* pc_d = nullptr;
+    double* col_d = nullptr;
+    double* wts_d = nullptr;
+    double* lampow_d = nullptr;
+    int lp_stride = 0;
+    cplx* tw_d = nullptr;
+    cplx* spec_d = nullptr;
+    double* xch_d = nullptr;
+    unsigned* flags_d = nullptr;
+    double* dw_d = nullptr;       // direct weights [B][N]
+    double* cprime_d = nullptr;   // [B][nodes]
+    double* den_d = nullptr;
+    double* scratch_d = nullptr;  // [B][nodes]
+    double* work_d = nullptr;     // staging for host buffers
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+uint64_t rows_of(const ft_plan* p) { return (uint64_t)p->B * (uint64_t)p->nodes; }
+
+// ---- reference setup restated (weights.cpp / schemes.cpp) -------------------
+double power_step(uint64_t k, double p) {  // weights.cpp:8-16
+    if (k == 0) return 1.0;
+    const double kd = (double)k;
+    if (k > 1000000) return std::pow(kd, p) * std::expm1(p * std::log1p(1.0 / kd));
+    return std::pow(kd + 1.0, p) - std::pow(kd, p);
+}
+
+int validate(const ft_problem& s) {  // schemes.cpp:58-78
+    const bool wave = s.scheme == FT_SCHEME_WAVE;
+    if (s.scheme != FT_SCHEME_ODE && s.scheme != FT_SCHEME_WAVE && s.scheme != FT_SCHEME_DIFFUSION)
+        return set_err(FT_EINVAL, "solve: unknown scheme");
+    if (wave) {
+        if (!(s.gamma > 1.0 && s.gamma < 2.0))
+            return set_err(FT_EINVAL, "ProblemSpec: wave scheme needs gamma in (1, 2)");
+    } else if (!(s.gamma > 0.0 && s.gamma < 1.0)) {
+        return set_err(FT_EINVAL, "ProblemSpec: scheme needs gamma in (0, 1)");
+    }
+    if (s.time_steps < 1) return set_err(FT_EINVAL, "ProblemSpec: need at least 1 time step");
+    if (s.scheme != FT_SCHEME_ODE && s.space_cells < 2)
+        return set_err(FT_EINVAL, "ProblemSpec: need at least 2 space cells");
+    if (!(s.time_length > 0.0) || (s.scheme != FT_SCHEME_ODE && !(s.space_length > 0.0)))
+        return set_err(FT_EINVAL, "ProblemSpec: domain lengths must be positive");
+    return FT_OK;
+}
+
+// Constant tridiagonal / upwind operator -> scan parameters (long double).
+void scan_params(ft_plan* p, int b, std::vector<double>& lampow) {
+    ProblemConst& pc = p->pc_h[b];
+    long double lam = 0.0L, phi = 0.0L;
+    if (p->kind == SK_TRIDIAG) {
+        const long double bb = (long double)pc.off;
+        const long double shift = (long double)pc.d - 2.0L * bb;  // exact
+        const long double delta = shift / (2.0L * bb);
+        phi = 2.0L * asinhl(sqrtl(delta / 2.0L));
+        lam = expl(-phi);
+        const long double one_m = -expm1l(-phi);
+        pc.lam = (double)lam;
+        pc.G0 = (double)(lam / (bb * one_m * (1.0L + lam)));
+        const long double Lam = expl(-phi * (long double)(p->nodes + 1));
+        pc.Lam = (double)Lam;
+        pc.inv1mL2 = (double)(1.0L / (1.0L - Lam * Lam));
+    } else if (p->kind == SK_UPWIND) {
+        lam = (long double)pc.off / (long double)pc.d;
+        pc.lam = (double)lam;
+        pc.G0 = (double)(1.0L / (long double)pc.d);
+        pc.Lam = 0.0;
+        pc.inv1mL2 = 1.0;
+    } else {
+        pc.lam = 0.0;
+        pc.G0 = 1.0 / pc.d;
+        pc.Lam = 0.0;
+        pc.inv1mL2 = 1.0;
+    }
+    double* lp = lampow.data() + (uint64_t)b * p->lp_stride;
+    for (int k = 0; k < p->lp_stride; ++k) {
+        long double v;
+        if (p->kind == SK_TRIDIAG) v = expl(-phi * (long double)k);
+        else if (p->kind == SK_UPWIND) v = powl(lam, (long double)k);
+        else v = k == 0 ? 1.0L : 0.0L;
+        lp[k] = (double)v;
+    }
+}
+
+void build_schedule(ft_plan* p) {
+    const uint64_t N = p->N, L = (uint64_t)p->L;
+    uint64_t Npad = L;
+    while (Npad < N) Npad <<= 1;
+    p->levels.clear();
+    uint64_t off = 0;
+    const int pairs = (p->nodes + 1) / 2 * p->B;
+    for (uint64_t n = 2 * L; n <= Npad; n <<= 1) {
+        Level lv;
+        lv.n = (int)n;
+        lv.K = n <= 16384 ? 2 : (int)(n / 8192);
+        lv.m = (int)(n / lv.K);
+        lv.G = lv.m >= kMpTile ? 1 : kMpTile / lv.m;
+        if (lv.G > pairs) lv.G = pairs;
+        lv.groups = (pairs + lv.G - 1) / lv.G;
+        lv.spec_off = off;
+        off += (uint64_t)p->B * n;
+        p->levels.push_back(lv);
+    }
+    int logT = 4;
+    while ((1ull << logT) < Npad) ++logT;
+    p->logT = logT;
+    p->ops.clear();
+    for (uint64_t t0 = 0; t0 < N; t0 += L) {
+        Op leaf{OP_LEAF, t0, (int)std::min<uint64_t>(L, N - t0), 0, 0, 0, t0 == 0};
+        p->ops.push_back(leaf);
+        const uint64_t t = t0 + L;
+        if (t >= N) break;
+        const uint64_t h = t & (~t + 1);  // lowest set bit
+        int level = 0;
+        while ((L << level) < h) ++level;
+        Op mp{OP_MP, t - h, 0, level, t, t + h, t - h == 0};
+        p->ops.push_back(mp);
+    }
+}
+
+int alloc_copy(void** dst, const void* src, size_t bytes) {
+    FT_CUDA(cudaMalloc(dst, bytes ? bytes : 8));
+    if (bytes && src) FT_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    return FT_OK;
+}
+
+bool is_device_ptr(const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int ensure_work(ft_plan* p) {
+    if (!p->work_d) FT_CUDA(cudaMalloc(&p->work_d, sizeof(double) * rows_of(p) * p->N));
+    return FT_OK;
+}
+
+int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, ft_plan** out) {
+    if (!probs || !out || count == 0) return set_err(FT_EINVAL, "ft_setup: null argument");
+    *out = nullptr;
+    for (uint64_t b = 0; b < count; ++b) {
+        int rc = validate(probs[b]);
+        if (rc) return rc;
+        const ft_problem& a = probs[b];
+        const ft_problem& z = probs[0];
+        if (a.scheme != z.scheme || a.time_steps != z.time_steps ||
+            (a.scheme != FT_SCHEME_ODE && a.space_cells != z.space_cells))
+            return set_err(FT_EINVAL, "ft_setup_batch: problems must share scheme, N and M");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(FT_ECUDA, "no CUDA device available (this library has no CPU path)");
+    }
+    ft_plan* p = new ft_plan();
+    const ft_problem& z = probs[0];
+    p->scheme = z.scheme;
+    p->B = (int)count;
+    p->N = z.time_steps;
+    p->cells = z.scheme == FT_SCHEME_ODE ? 0 : z.space_cells;
+    p->nodes = z.scheme == FT_SCHEME_ODE ? 1 : (int)(z.space_cells - 1);
+    p->tau = z.time_length / (double)z.time_steps;
+    p->h = z.scheme == FT_SCHEME_ODE ? 0.0 : z.space_length / (double)z.space_cells;
+    p->rhs_mode = opt ? opt->rhs_mode : 0;
+    p->J = (opt && opt->near_field > 0) ? opt->near_field : (z.scheme == FT_SCHEME_WAVE ? 64 : 1);
+    if (opt && opt->device >= 0) FT_CUDA(cudaSetDevice(opt->device));
+    FT_CUDA(cudaGetDevice(&p->device));
+
+    const uint64_t N = p->N;
+    p->kind = z.scheme == FT_SCHEME_ODE ? SK_DIAG : z.scheme == FT_SCHEME_WAVE ? SK_UPWIND : SK_TRIDIAG;
+    p->gamma.resize(count);
+    p->mu.resize(count);
+    p->c.resize(count);
+    p->col_h.assign(count * N, 0.0);
+    p->wts_h.assign(count * (N + 1), 0.0);
+    p->pc_h.resize(count);
+    std::vector<double> dw(count * N, 0.0), cprime, den;
+    if (p->kind == SK_TRIDIAG) {
+        cprime.assign(count * p->nodes, 0.0);
+        den.assign(count * p->nodes, 0.0);
+    }
+    for (uint64_t b = 0; b < count; ++b) {
+        const double g = probs[b].gamma;
+        const double tau = probs[b].time_length / (double)probs[b].time_steps;
+        const double h = p->h;
+        p->gamma[b] = g;
+        // SchemeConstants::for_spec (schemes.cpp:44-56)
+        const double mu = std::pow(tau, -g) / std::tgamma(2.0 - g);
+        double c = mu;
+        if (p->scheme == FT_SCHEME_WAVE) c = std::pow(tau, -g) / std::tgamma(3.0 - g);
+        if (p->scheme == FT_SCHEME_DIFFUSION) c = std::pow(tau, -g) / std::tgamma(2.0 - g);
+        p->mu[b] = mu;
+        p->c[b] = c;
+        double* col = p->col_h.data() + b * N;
+        double* wv = p->wts_h.data() + b * (N + 1);
+        ProblemConst& pc = p->pc_h[b];
+        pc.c = c;
+        pc.h = h;
+        if (p->scheme == FT_SCHEME_WAVE) {
+            // m_weights(gamma, N+1) and assemble_scheme3_reordered (schemes.cpp:277-287)
+            for (uint64_t k = 0; k <= N; ++k) wv[k] = power_step(k, 2.0 - g);
+            col[0] = 1.0 / h + c * wv[0];
+            if (N > 1) col[1] = c * (wv[1] - 2.0 * wv[0]);
+            for (uint64_t j = 2; j < N; ++j) col[j] = c * (wv[j - 2] - 2.0 * wv[j - 1] + wv[j]);
+            pc.d = c * wv[0] + 1.0 / h;  // schemes.cpp:348 denominator
+            pc.off = 1.0 / h;
+            for (uint64_t j = 0; j < N; ++j) dw[b * N + j] = col[j];
+        } else {
+            // g_weights(gamma, N) (+1 spare for the RHS kernel)
+            for (uint64_t k = 0; k <= N; ++k) wv[k] = power_step(k, 1.0 - g);
+            if (p->scheme == FT_SCHEME_DIFFUSION) {
+                col[0] = 2.0 / (h * h) + c * wv[0];  // schemes.cpp:394-396
+                for (uint64_t j = 1; j < N; ++j) col[j] = c * (wv[j] - wv[j - 1]);
+                pc.d = col[0];
+                pc.off = 1.0 / (h * h);
+                for (uint64_t j = 1; j < N; ++j) dw[b * N + j] = wv[j - 1] - wv[j];
+                // Thomas factors, schemes.cpp:453-460 (same expressions, same order)
+                const double diag = 2.0 / (h * h) + c * wv[0];
+                const double off = -1.0 / (h * h);
+                double denom = diag;
+                cprime[b * p->nodes] = off / denom;
+                den[b * p->nodes] = denom;
+                for (int i = 1; i < p->nodes; ++i) {
+                    denom = diag - off * cprime[b * p->nodes + i - 1];
+                    cprime[b * p->nodes + i] = off / denom;
+                    den[b * p->nodes + i] = denom;
+                }
+            } else {
+                col[0] = 1.0 + mu * wv[0];  // SURVEY.md 3.4 composition
+                for (uint64_t j = 1; j < N; ++j) col[j] = mu * (wv[j] - wv[j - 1]);
+                pc.d = col[0];
+                pc.off = 0.0;
+                for (uint64_t j = 0; j < N; ++j) dw[b * N + j] = col[j];
+            }
+        }
+    }
+
+    // leaf configuration
+    const int nodes = p->nodes;
+    if (p->kind == SK_DIAG) {
+        p->npt = 1; p->L = 32; p->threads = 32; p->slab = 1; p->P = 1;
+    } else if (nodes <= 256) {
+        p->npt = 1; p->L = 32; p->threads = ((nodes + 31) / 32) * 32; p->slab = nodes; p->P = 1;
+    } else if (nodes <= 512) {
+        p->npt = 2; p->L = 32; p->threads = ((nodes + 63) / 64) * 32; p->slab = nodes; p->P = 1;
+    } else if (nodes <= 1024) {
+        p->npt = 4; p->L = 16; p->threads = ((nodes + 127) / 128) * 32; p->slab = nodes; p->P = 1;
+    } else if (nodes <= 2048) {
+        p->npt = 8; p->L = 8; p->threads = ((nodes + 255) / 256) * 32; p->slab = nodes; p->P = 1;
+    } else {
+        p->npt = 2; p->L = 32; p->threads = 256; p->slab = 512;
+        p->P = (nodes + p->slab - 1) / p->slab;
+        p->multi = true;
+        int dev_sms = 0;
+        FT_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
+        if ((int64_t)p->P * p->B > dev_sms) {
+            delete p;
+            return set_err(FT_EINVAL, "ft_setup: spatial slabs exceed co-resident CTAs "
+                                      "(reduce the batch or the node count per problem)");
+        }
+    }
+    p->lp_stride = std::max(nodes + 2, 4098);
+    std::vector<double> lampow((uint64_t)count * p->lp_stride);
+    for (uint64_t b = 0; b < count; ++b) scan_params(p, (int)b, lampow);
+    build_schedule(p);
+
+    // device copies
+    const uint64_t B = count;
+    int rc;
+    if ((rc = alloc_copy((void**)&p->pc_d, p->pc_h.data(), sizeof(ProblemConst) * B))) return rc;
+    if ((rc = alloc_copy((void**)&p->col_d, p->col_h.data(), sizeof(double) * B * N))) return rc;
+    if ((rc = alloc_copy((void**)&p->wts_d, p->wts_h.data(), sizeof(double) * B * (N + 1)))) return rc;
+    if ((rc = alloc_copy((void**)&p->lampow_d, lampow.data(), sizeof(double) * lampow.size()))) return rc;
+    if ((rc = alloc_copy((void**)&p->dw_d, dw.data(), sizeof(double) * dw.size()))) return rc;
+    if (p->kind == SK_TRIDIAG) {
+        if ((rc = alloc_copy((void**)&p->cprime_d, cprime.data(), sizeof(double) * cprime.size()))) return rc;
+        if ((rc = alloc_copy((void**)&p->den_d, den.data(), sizeof(double) * den.size()))) return rc;
+    }
+    if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * B * nodes))) return rc;
+    if (p->multi) {
+        if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 4 * B * p->P))) return rc;
+        if ((rc = alloc_copy((void**)&p->flags_d, nullptr, sizeof(unsigned) * B * p->P))) return rc;
+    }
+    // twiddles exp(-2 pi i k / T), long double
+    {
+        const uint64_t T = 1ull << p->logT;
+        std::vector<cplx> tw(T);
+        const long double pi = 3.141592653589793238462643383279502884L;
+        for (uint64_t k = 0; k < T; ++k) {
+            const long double ang = 2.0L * pi * (long double)k / (long double)T;
+            tw[k] = {(double)cosl(ang), (double)(-sinl(ang))};
+        }
+        if ((rc = alloc_copy((void**)&p->tw_d, tw.data(), sizeof(cplx) * T))) return rc;
+    }
+    FT_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+    FT_CUDA(cudaEventCreate(&p->ev0));
+    FT_CUDA(cudaEventCreate(&p->ev1));
+    // kernel spectra per level (embed_circulant equivalent)
+    uint64_t spec_total = 0;
+    for (auto& lv : p->levels) spec_total += (uint64_t)B * lv.n;
+    if ((rc = alloc_copy((void**)&p->spec_d, nullptr, sizeof(cplx) * std::max<uint64_t>(spec_total, 1)))) return rc;
+    for (auto& lv : p->levels) {
+        FT_CUDA(launch_spectra(p->col_d, N, (int)B, lv.n, lv.m, lv.K, p->J, p->spec_d + lv.spec_off,
+                               p->tw_d, p->logT, p->stream));
+    }
+    FT_CUDA(cudaStreamSynchronize(p->stream));
+    *out = p;
+    return FT_OK;
+}
+
+int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches) {
+    const cudaStream_t st = p->stream;
+    const uint64_t N = p->N;
+    if (p->multi) FT_CUDA(cudaMemsetAsync(p->flags_d, 0, sizeof(unsigned) * p->B * p->P, st));
+    unsigned step_base = 0;
+    uint64_t nl = 0;
+    for (const Op& op : p->ops) {
+        if (op.kind == OP_LEAF) {
+            LeafArgs a;
+            a.X = X;
+            a.src = op.first ? rhs : X;
+            a.N = N;
+            a.t0 = op.t0;
+            a.len = op.len;
+            a.nodes = p->nodes;
+            a.slab = p->slab;
+            a.P = p->P;
+            a.pc = p->pc_d;
+            a.col = p->col_d;
+            a.lampow = p->lampow_d;
+            a.lp_stride = p->lp_stride;
+            a.xch = p->xch_d;
+            a.flags = p->flags_d;
+            a.step_base = step_base;
+            FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P, p->threads, st));
+            step_base += (unsigned)op.len;
+        } else {
+            const Level& lv = p->levels[op.level];
+            MpArgs a;
+            a.X = X;
+            a.rsrc = op.first ? rhs : X;
+            a.N = N;
+            a.lo = op.t0;
+            a.mid = op.mid;
+            a.hi = op.hi;
+            a.n = lv.n;
+            a.m = lv.m;
+            a.K = lv.K;
+            a.G = lv.G;
+            a.rows = (int)rows_of(p);
+            a.nodes = p->nodes;
+            a.pairs_per_problem = (p->nodes + 1) / 2;
+            a.spec = p->spec_d + lv.spec_off;
+            a.tw = p->tw_d;
+            a.logT = p->logT;
+            a.col = p->col_d;
+            a.J = p->J;
+            FT_CUDA(launch_mp(a, lv.groups, st));
+        }
+        ++nl;
+    }
+    if (launches) *launches = nl;
+    return FT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ft_last_error(void) { return g_err.c_str(); }
+
+int ft_setup(const ft_problem* problem, const ft_options* options, ft_plan** out) {
+    return setup_impl(problem, 1, options, out);
+}
+
+int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options* options,
+                   ft_plan** out) {
+    return setup_impl(problems, count, options, out);
+}
+
+int ft_plan_get_info(const ft_plan* p, ft_plan_info* info) {
+    if (!p || !info) return set_err(FT_EINVAL, "ft_plan_get_info: null argument");
+    info->problems = p->B;
+    info->nodes = p->nodes;
+    info->time_steps = p->N;
+    info->leaf = p->L;
+    info->levels = p->levels.size();
+    info->slabs = p->P;
+    info->h = p->h;
+    info->tau = p->tau;
+    info->mu = p->mu[0];
+    info->c = p->c[0];
+    return FT_OK;
+}
+
+int ft_column(const ft_plan* p, uint64_t problem, double* col) {
+    if (!p || !col || problem >= (uint64_t)p->B) return set_err(FT_EINVAL, "ft_column: bad argument");
+    std::memcpy(col, p->col_h.data() + problem * p->N, sizeof(double) * p->N);
+    return FT_OK;
+}
+
+int ft_set_stream(ft_plan* p, void* s) {
+    if (!p) return set_err(FT_EINVAL, "ft_set_stream: null plan");
+    if (p->own_stream) cudaStreamDestroy(p->stream);
+    p->stream = (cudaStream_t)s;
+    p->own_stream = false;
+    return FT_OK;
+}
+
+// assemble_scheme4 rhs (schemes.cpp:401-408) / Scheme3Rhs (:300-306) / ODE
+int ft_assemble_rhs(const ft_plan* p, ft_forcing_fn f, ft_initial_fn u0, ft_initial_fn phi,
+                    void* user, double* rhs) {
+    if (!p || !rhs) return set_err(FT_EINVAL, "ft_assemble_rhs: null argument");
+    if (!f) return set_err(FT_EINVAL, "ProblemSpec: forcing callback is required");
+    const uint64_t N = p->N;
+    for (int b = 0; b < p->B; ++b) {
+        const double c = p->c[b], tau = p->tau, h = p->h;
+        const double* w = p->wts_h.data() + (uint64_t)b * (N + 1);
+        for (int i = 1; i <= p->nodes; ++i) {
+            const double x = p->scheme == FT_SCHEME_ODE ? 0.0 : (double)i * h;
+            const double u = u0 ? u0(x, user) : 0.0;
+            const double ph = phi ? phi(x, user) : 0.0;
+            double* r = rhs + ((uint64_t)b * p->nodes + (i - 1)) * N;
+            for (uint64_t n = 1; n <= N; ++n) {
+                if (p->scheme == FT_SCHEME_WAVE) {
+                    const double t_half = ((double)n - 0.5) * tau;
+                    double value = f(x, t_half, user) + c * tau * w[n - 1] * ph;
+                    if (n >= 2) value -= c * (w[n - 2] - w[n - 1]) * u;
+                    else if (p->rhs_mode == FT_RHS_CORRECTED_N1) value += c * w[0] * u;
+                    r[n - 1] = value;
+                } else {
+                    r[n - 1] = f(x, (double)n * tau, user) + c * w[n - 1] * u;
+                }
+            }
+        }
+    }
+    return FT_OK;
+}
+
+int ft_assemble_rhs_grid(const ft_plan* p, const double* F, const double* u0, const double* phi,
+                         double* rhs) {
+    if (!p || !F || !rhs) return set_err(FT_EINVAL, "ft_assemble_rhs_grid: null argument");
+    if (is_device_ptr(F) || is_device_ptr(rhs))
+        return set_err(FT_EINVAL, "ft_assemble_rhs_grid: host arrays expected");
+    const uint64_t N = p->N;
+    for (int b = 0; b < p->B; ++b) {
+        const double c = p->c[b], tau = p->tau;
+        const double* w = p->wts_h.data() + (uint64_t)b * (N + 1);
+        for (int i = 0; i < p->nodes; ++i) {
+            const uint64_t row = (uint64_t)b * p->nodes + i;
+            const double u = u0 ? u0[row] : 0.0;
+            const double ph = phi ? phi[row] : 0.0;
+            const double* Fr = F + row * N;
+            double* r = rhs + row * N;
+            for (uint64_t n = 1; n <= N; ++n) {
+                if (p->scheme == FT_SCHEME_WAVE) {
+                    double value = Fr[n - 1] + c * tau * w[n - 1] * ph;
+                    if (n >= 2) value -= c * (w[n - 2] - w[n - 1]) * u;
+                    else if (p->rhs_mode == FT_RHS_CORRECTED_N1) value += c * w[0] * u;
+                    r[n - 1] = value;
+                } else {
+                    r[n - 1] = Fr[n - 1] + c * w[n - 1] * u;
+                }
+            }
+        }
+    }
+    return FT_OK;
+}
+
+int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const double* k,
+                          const double* pe, const int* trig, const double* u0amp,
+                          const double* phiamp, double* rhs) {
+    if (!p || !rhs || nmodes < 0 || (nmodes && (!a || !k || !pe || !trig)))
+        return set_err(FT_EINVAL, "ft_assemble_rhs_modes: bad argument");
+    if (!is_device_ptr(rhs)) return set_err(FT_EINVAL, "ft_assemble_rhs_modes: rhs must be device memory");
+    FT_CUDA(cudaSetDevice(p->device));
+    const int B = p->B;
+    std::vector<double> cv(B);
+    for (int b = 0; b < B; ++b) cv[b] = p->c[b];
+    double *a_d, *k_d, *p_d, *c_d, *u_d = nullptr, *f_d = nullptr;
+    int* t_d;
+    int rc;
+    if ((rc = alloc_copy((void**)&a_d, a, sizeof(double) * B * nmodes))) return rc;
+    if ((rc = alloc_copy((void**)&k_d, k, sizeof(double) * nmodes))) return rc;
+    if ((rc = alloc_copy((void**)&p_d, pe, sizeof(double) * B * nmodes))) return rc;
+    if ((rc = alloc_copy((void**)&t_d, trig, sizeof(int) * nmodes))) return rc;
+    if ((rc = alloc_copy((void**)&c_d, cv.data(), sizeof(double) * B))) return rc;
+    if (u0amp && (rc = alloc_copy((void**)&u_d, u0amp, sizeof(double) * B))) return rc;
+    if (phiamp && (rc = alloc_copy((void**)&f_d, phiamp, sizeof(double) * B))) return rc;
+    RhsModesArgs ra;
+    ra.R = rhs;
+    ra.N = p->N;
+    ra.nodes = p->nodes;
+    ra.B = B;
+    ra.nmodes = nmodes;
+    ra.scheme = p->scheme;
+    ra.rhs_mode = p->rhs_mode;
+    ra.h = p->h;
+    ra.tau = p->tau;
+    ra.a = a_d;
+    ra.k = k_d;
+    ra.p = p_d;
+    ra.trig = t_d;
+    ra.u0amp = u_d;
+    ra.phiamp = f_d;
+    ra.wts = p->wts_d;
+    ra.cvals = c_d;
+    FT_CUDA(launch_rhs_modes(ra, p->stream));
+    FT_CUDA(cudaStreamSynchronize(p->stream));
+    cudaFree(a_d); cudaFree(k_d); cudaFree(p_d); cudaFree(t_d); cudaFree(c_d);
+    if (u_d) cudaFree(u_d);
+    if (f_d) cudaFree(f_d);
+    return FT_OK;
+}
+
+static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool fast) {
+    if (!p || !rhs || !u) return set_err(FT_EINVAL, "ft_solve: null argument");
+    const auto t_start = std::chrono::steady_clock::now();
+    FT_CUDA(cudaSetDevice(p->device));
+    const uint64_t elems = rows_of(p) * p->N;
+    const size_t bytes = sizeof(double) * elems;
+    const bool rhs_dev = is_device_ptr(rhs), u_dev = is_device_ptr(u);
+    const cudaStream_t st = p->stream;
+    double* X;
+    const double* src;
+    if (u_dev) {
+        X = u;
+        if (rhs_dev) {
+            src = rhs;
+        } else {
+            FT_CUDA(cudaMemcpyAsync(X, rhs, bytes, cudaMemcpyHostToDevice, st));
+            src = X;
+        }
+    } else {
+        int rc = ensure_work(p);
+        if (rc) return rc;
+        X = p->work_d;
+        if (rhs_dev) {
+            src = rhs;
+        } else {
+            FT_CUDA(cudaMemcpyAsync(X, rhs, bytes, cudaMemcpyHostToDevice, st));
+            src = X;
+        }
+    }
+    uint64_t launches = 0;
+    FT_CUDA(cudaEventRecord(p->ev0, st));
+    if (fast) {
+        int rc = run_fast(p, X, src, &launches);
+        if (rc) return rc;
+    } else {
+        if (src != X) FT_CUDA(cudaMemcpyAsync(X, src, bytes, cudaMemcpyDeviceToDevice, st));
+        DirectArgs da;
+        da.X = X;
+        da.N = p->N;
+        da.nodes = p->nodes;
+        da.kind = p->kind;
+        da.w = p->dw_d;
+        da.cprime = p->cprime_d;
+        da.den = p->den_d;
+        da.pc = p->pc_d;
+        da.scratch = p->scratch_d;
+        FT_CUDA(launch_direct(da, p->B, st));
+        launches = 1;
+    }
+    FT_CUDA(cudaEventRecord(p->ev1, st));
+    if (!u_dev) FT_CUDA(cudaMemcpyAsync(u, X, bytes, cudaMemcpyDeviceToHost, st));
+    FT_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    FT_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    if (rep) {
+        std::snprintf(rep->method, sizeof(rep->method), "%s", fast ? "fast" : "direct");
+        rep->iterations = 0;
+        rep->residual = 0.0;
+        rep->device_ms = ms;
+        rep->kernel_launches = launches;
+        rep->seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+    return FT_OK;
+}
+
+int ft_solve_fast(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
+    return solve_common(p, rhs, u, rep, true);
+}
+
+int ft_solve_direct(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
+    return solve_common(p, rhs, u, rep, false);
+}
+
+void ft_destroy(ft_plan* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
+                    p->flags_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+}
+
+}  // extern "C"

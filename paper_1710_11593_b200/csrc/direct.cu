@@ -1,0 +1,117 @@
+// direct.cu -- the "direct" entry point on the GPU: time marching in the
+// reference's summation order (compiled with --fmad=false so every product
+// and sum rounds exactly as the reference's x86-64 build does), plus device
+// generation of separable right-hand sides.
+//
+//   Scheme 4 direct : src/schemes.cpp:434-463  (history :447-449, Thomas :453-461)
+//   Scheme 3 direct : src/schemes.cpp:333-352  (history :336-343, upwind march :345-351)
+//   ODE direct      : src/toeplitz.cpp:169-186 (lower_toeplitz_forward_solve)
+//   RHS             : src/schemes.cpp:401-408 (Scheme 4), :300-306 (Scheme3Rhs)
+#include "internal.cuh"
+
+namespace ftb {
+
+// One CTA per problem; the step loop runs inside the kernel.
+__global__ void __launch_bounds__(1024) direct_kernel(DirectArgs a) {
+    const int pb = blockIdx.x;
+    const uint64_t N = a.N;
+    const int nodes = a.nodes;
+    double* X = a.X + (uint64_t)pb * nodes * N;
+    const double* w = a.w + (uint64_t)pb * N;
+    double* rhs = a.scratch + (uint64_t)pb * nodes;
+    const ProblemConst pc = a.pc[pb];
+    for (uint64_t n = 0; n < N; ++n) {
+        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
+            const double* xi = X + (uint64_t)i * N;
+            if (a.kind == SK_TRIDIAG) {
+                // hist = sum_{k=1}^{n-1} (g[n-k-1] - g[n-k]) U(i,k)  (1-based n, k)
+                double hist = 0.0;
+                for (uint64_t k = 0; k < n; ++k) hist += w[n - k] * xi[k];
+                rhs[i] = xi[n] + pc.c * hist;
+            } else if (a.kind == SK_UPWIND) {
+                double hist = 0.0;
+                if (n >= 1) {
+                    hist += w[1] * xi[n - 1];
+                    for (uint64_t k = 0; k + 1 < n; ++k) hist += w[n - k] * xi[k];
+                }
+                rhs[i] = xi[n] - hist;
+            } else {
+                double acc = xi[n];
+                for (uint64_t k = 0; k < n; ++k) acc -= w[n - k] * xi[k];
+                rhs[i] = acc;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double* cp = a.cprime + (uint64_t)pb * nodes;
+            const double* dn = a.den + (uint64_t)pb * nodes;
+            if (a.kind == SK_TRIDIAG) {
+                const double off = -pc.off;
+                rhs[0] /= dn[0];
+                for (int i = 1; i < nodes; ++i) rhs[i] = (rhs[i] - off * rhs[i - 1]) / dn[i];
+                for (int i = nodes - 1; i-- > 0;) rhs[i] -= cp[i] * rhs[i + 1];
+            } else if (a.kind == SK_UPWIND) {
+                double u_left = 0.0;
+                for (int i = 0; i < nodes; ++i) {
+                    const double value = (rhs[i] + u_left / pc.h) / pc.d;
+                    rhs[i] = value;
+                    u_left = value;
+                }
+            } else {
+                for (int i = 0; i < nodes; ++i) rhs[i] = rhs[i] / pc.d;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nodes; i += blockDim.x) X[(uint64_t)i * N + n] = rhs[i];
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st) {
+    int threads = a.nodes < 1024 ? ((a.nodes + 31) / 32) * 32 : 1024;
+    direct_kernel<<<B, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---- device RHS generation (separable forcing) -------------------------------
+__global__ void rhs_modes_kernel(RhsModesArgs a) {
+    const uint64_t total = (uint64_t)a.B * a.nodes * a.N;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t n0 = idx % a.N;
+        const uint64_t row = idx / a.N;
+        const int pb = (int)(row / a.nodes);
+        const int i = (int)(row % a.nodes) + 1;
+        const double x = a.scheme == 0 ? 0.0 : (double)i * a.h;
+        const double n = (double)(n0 + 1);
+        const double t = a.scheme == 2 ? (n - 0.5) * a.tau : n * a.tau;
+        double f = 0.0;
+        for (int j = 0; j < a.nmodes; ++j) {
+            const int tg = a.trig[j];
+            const double sp = tg == 0 ? sin(a.k[j] * 3.14159265358979323846 * x)
+                              : tg == 1 ? cos(a.k[j] * 3.14159265358979323846 * x)
+                                        : 1.0;
+            f += a.a[pb * a.nmodes + j] * sp * pow(t, a.p[pb * a.nmodes + j]);
+        }
+        const double* wv = a.wts + (uint64_t)pb * (a.N + 1);
+        const double c = a.cvals[pb];
+        const double u0 = a.u0amp ? a.u0amp[pb] * (a.scheme == 0 ? 1.0 : sin(3.14159265358979323846 * x)) : 0.0;
+        double v;
+        if (a.scheme == 2) {
+            const double phi = a.phiamp ? a.phiamp[pb] * sin(3.14159265358979323846 * x) : 0.0;
+            v = f + c * a.tau * wv[n0] * phi;
+            if (n0 >= 1) v -= c * (wv[n0 - 1] - wv[n0]) * u0;
+            else if (a.rhs_mode == 1) v += c * wv[0] * u0;
+        } else {
+            v = f + c * wv[n0] * u0;
+        }
+        a.R[idx] = v;
+    }
+}
+
+cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st) {
+    rhs_modes_kernel<<<148 * 8, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ftb

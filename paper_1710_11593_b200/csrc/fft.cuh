@@ -1,0 +1,179 @@
+// fft.cuh -- batched fp64 complex FFT in shared memory (in-place radix-16/8/4/2
+// passes, data staged through registers).  Forward = decimation in frequency
+// (natural order in, digit-reversed order out); inverse = decimation in time
+// (digit-reversed in, natural out).  Convolutions multiply spectra pointwise
+// in the digit-reversed domain, so no reordering pass exists anywhere.  The
+// kernel spectra are produced by the same forward routine, so their order
+// matches by construction.
+//
+// Replaces the reference's radix-2 bit-reversal FFT (src/fft.cpp:50-79) as the
+// arithmetic of the history product; see DESIGN.md for the pass plan.
+#pragma once
+#include "internal.cuh"
+
+namespace ftb {
+
+// Shared-memory index padding: one pad slot per 16 complex values keeps the
+// radix-16 column reads of the last pass conflict-free.
+__device__ __forceinline__ int sphys(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int spad_len(int n) { return n + (n >> 4) + 1; }
+
+// cos(2*pi*k/16), k = 0..15 (compile-time k after unrolling)
+__device__ __forceinline__ double c16(int k) {
+    switch (k & 15) {
+        case 0: return 1.0;
+        case 1: case 15: return 0.92387953251128675613;
+        case 2: case 14: return 0.70710678118654752440;
+        case 3: case 13: return 0.38268343236508977173;
+        case 4: case 12: return 0.0;
+        case 5: case 11: return -0.38268343236508977173;
+        case 6: case 10: return -0.70710678118654752440;
+        case 7: case 9: return -0.92387953251128675613;
+        default: return -1.0;
+    }
+}
+
+// multiply by w_S^i = exp(-+2 pi i * i / S) for S | 16 (compile-time i, S)
+template <int S, bool INV>
+__device__ __forceinline__ cplx twc(cplx v, int i) {
+    const int k = i * (16 / S);  // angle 2 pi k / 16, k in [0, 8)
+    if (k == 0) return v;
+    if (k == 4) return INV ? cplx{-v.y, v.x} : cplx{v.y, -v.x};
+    const double c = c16(k);
+    const double s = c16((k + 12) & 15);  // sin(2 pi k/16) = cos(2 pi (k-4)/16)
+    // forward: (x + iy)(c - is);  inverse: (x + iy)(c + is)
+    if (INV) return {fma(v.x, c, -v.y * s), fma(v.y, c, v.x * s)};
+    return {fma(v.x, c, v.y * s), fma(v.y, c, -v.x * s)};
+}
+
+template <int R>
+__device__ __forceinline__ constexpr int bitrev(int q) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r = (r << 1) | (q & 1);
+        q >>= 1;
+    }
+    return r;
+}
+
+// In-register R-point DFT, natural order in and out.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
+#pragma unroll
+    for (int s = R / 2; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int b = 0; b < R; b += 2 * s) {
+#pragma unroll
+            for (int i = 0; i < s; ++i) {
+                const cplx a = v[b + i], c = v[b + i + s];
+                v[b + i] = cadd(a, c);
+                const cplx d = csub(a, c);
+                if (s == 1) v[b + i + s] = d;
+                else if (s == 2) v[b + i + s] = twc<4, INV>(d, i);
+                else if (s == 4) v[b + i + s] = twc<8, INV>(d, i);
+                else v[b + i + s] = twc<16, INV>(d, i);
+            }
+        }
+    }
+    cplx t[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) t[q] = v[bitrev<R>(q)];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = t[q];
+}
+
+// One in-place DIF pass over all sequences of `total` points, group size S.
+template <int R>
+__device__ __forceinline__ void fwd_pass(cplx* buf, int total, int S, const cplx* __restrict__ tw,
+                                         int logT, int logS) {
+    const int Q = S / R;
+    const int tasks = total / R;
+    for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+        const int j = t & (Q - 1);
+        const int base = (t / Q) * S + j;
+        cplx v[R];
+#pragma unroll
+        for (int p = 0; p < R; ++p) v[p] = buf[sphys(base + p * Q)];
+        dft_reg<R, false>(v);
+        if (Q > 1) {
+            const int sh = logT - logS;
+#pragma unroll
+            for (int q = 1; q < R; ++q) v[q] = cmul(v[q], ldgc(&tw[(j * q) << sh]));
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) buf[sphys(base + q * Q)] = v[q];
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void inv_pass(cplx* buf, int total, int S, const cplx* __restrict__ tw,
+                                         int logT, int logS) {
+    const int Q = S / R;
+    const int tasks = total / R;
+    for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+        const int j = t & (Q - 1);
+        const int base = (t / Q) * S + j;
+        cplx v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = buf[sphys(base + q * Q)];
+        if (Q > 1) {
+            const int sh = logT - logS;
+#pragma unroll
+            for (int q = 1; q < R; ++q) v[q] = cmulc(v[q], ldgc(&tw[(j * q) << sh]));
+        }
+        dft_reg<R, true>(v);
+#pragma unroll
+        for (int p = 0; p < R; ++p) buf[sphys(base + p * Q)] = v[p];
+    }
+}
+
+// radix of the first (largest-S) pass for an m-point transform; the rest are 16
+__device__ __forceinline__ int first_radix(int logm) {
+    const int r = logm & 3;
+    return r == 0 ? 16 : (1 << r);
+}
+
+// Forward transform of G sequences of m = 2^logm points (total = G*m) in buf.
+// Caller synchronises before (data written) and after (data read).
+__device__ __forceinline__ void fft_forward(cplx* buf, int total, int logm, const cplx* tw,
+                                            int logT) {
+    int logS = logm;
+    bool first = true;
+    while (logS > 0) {
+        const int R = first ? first_radix(logm) : 16;
+        const int S = 1 << logS;
+        switch (R) {
+            case 16: fwd_pass<16>(buf, total, S, tw, logT, logS); break;
+            case 8: fwd_pass<8>(buf, total, S, tw, logT, logS); break;
+            case 4: fwd_pass<4>(buf, total, S, tw, logT, logS); break;
+            default: fwd_pass<2>(buf, total, S, tw, logT, logS); break;
+        }
+        __syncthreads();
+        logS -= (R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1);
+        first = false;
+    }
+}
+
+__device__ __forceinline__ void fft_inverse(cplx* buf, int total, int logm, const cplx* tw,
+                                            int logT) {
+    // passes in reverse order: group sizes 16, 256, ... then the first-radix pass at S = m
+    const int r0 = first_radix(logm);
+    const int l0 = r0 == 16 ? 4 : r0 == 8 ? 3 : r0 == 4 ? 2 : 1;
+    int logS = (logm - l0) == 0 ? logm : 4;
+    while (true) {
+        const bool last = (logS == logm);
+        const int R = last ? r0 : 16;
+        const int S = 1 << logS;
+        switch (R) {
+            case 16: inv_pass<16>(buf, total, S, tw, logT, logS); break;
+            case 8: inv_pass<8>(buf, total, S, tw, logT, logS); break;
+            case 4: inv_pass<4>(buf, total, S, tw, logT, logS); break;
+            default: inv_pass<2>(buf, total, S, tw, logT, logS); break;
+        }
+        __syncthreads();
+        if (last) break;
+        logS = (logS + 4 <= logm - l0) ? logS + 4 : logm;
+    }
+}
+
+}  // namespace ftb

@@ -1,0 +1,124 @@
+// internal.cuh -- shared definitions of the B200 fast BLTT solver.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ftb {
+
+// Spatial operator of one time step (the diagonal block  col0*I + spatial part):
+//   SK_DIAG    : d x = r                                  (one-sided ODE)
+//   SK_UPWIND  : d x_i - s x_{i-1} = r_i,  x_0 = 0          (reference Scheme 3, s = 1/h)
+//   SK_TRIDIAG : d x_i - b (x_{i-1} + x_{i+1}) = r_i, Dirichlet  (reference Scheme 4, b = 1/h^2)
+enum SpaceKind { SK_DIAG = 0, SK_UPWIND = 1, SK_TRIDIAG = 2 };
+
+// Per-problem constants of the step operator, in the form the scan solver
+// uses.  TRIDIAG: x = G0 (F + B - r) + alpha lam^i + gam lam^(n+1-i)
+// with F/B the forward/backward lam-decay scans of r.  UPWIND: x = F where F is
+// the forward scan with multiplier lam = s/d of  r/d.
+struct ProblemConst {
+    double d;        // col[0]
+    double off;      // b (tridiag) or s (upwind), positive
+    double lam;      // decay multiplier
+    double G0;       // tridiag Green normalisation (upwind: 1/d)
+    double Lam;      // lam^(nodes+1)
+    double inv1mL2;  // 1/(1-Lam^2)
+    double c;        // scheme constant c (direct path)
+    double h;        // mesh width (direct wave path divides by it, as the reference)
+};
+
+constexpr int kLeafThreads = 256;
+constexpr int kMpThreads = 256;
+constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
+
+struct __align__(16) cplx {
+    double x, y;
+};
+
+__host__ __device__ inline cplx cmul(cplx a, cplx b) {
+    return {fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+__host__ __device__ inline cplx cmulc(cplx a, cplx b) {  // a * conj(b)
+    return {fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y)};
+}
+__device__ __forceinline__ cplx ldgc(const cplx* p) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    return {v.x, v.y};
+}
+__host__ __device__ inline cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
+__host__ __device__ inline cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
+
+// ---- launch arguments ------------------------------------------------------
+
+struct LeafArgs {
+    double* X;                 // rows x N, node-major (U for solved steps, R after)
+    const double* src;         // where this leaf's R tile is read from (X or the caller's rhs)
+    uint64_t N;                // row pitch = time steps
+    uint64_t t0;               // first step of the leaf
+    int len;                   // steps in this leaf (<= L)
+    int nodes;                 // interior nodes per problem
+    int slab;                  // nodes per CTA
+    int P;                     // slabs (CTAs) per problem
+    const ProblemConst* pc;    // [B]
+    const double* col;         // [B][N] Toeplitz first columns
+    const double* lampow;      // [B][lp_stride]: lam^k, k = 0..lp_stride-1
+    int lp_stride;
+    double* xch;               // multi-slab exchange [2][B*P][2]
+    unsigned* flags;           // [B*P] step flags (multi-slab)
+    unsigned step_base;        // steps completed before this leaf in the current solve
+};
+
+struct MpArgs {
+    double* X;
+    const double* rsrc;        // target R is read from here (== X except first touch)
+    uint64_t N;
+    uint64_t lo, mid, hi;      // source [lo, mid), target [mid, min(hi, N))
+    int n, m, K, G;            // block size, branch length, branches, row pairs per CTA
+    int rows, nodes;           // total rows, nodes per problem
+    int pairs_per_problem;
+    const cplx* spec;          // spectra of this level: [B][K][m] digit-reversed, scaled 1/n
+    const cplx* tw;            // twiddle table w_T^k = exp(-2 pi i k / T)
+    int logT;
+    const double* col;         // [B][N] (near field)
+    int J;                     // near-field lags summed exactly: 1..J-1
+};
+
+struct DirectArgs {
+    double* X;            // in: R (node-major), out: U; in place
+    uint64_t N;
+    int nodes;
+    int kind;             // SK_*
+    const double* w;      // [B][N]: S4 dg[j] = g[j-1]-g[j]; S3/ODE: col[j]
+    const double* cprime; // [B][nodes] Thomas (S4)
+    const double* den;    // [B][nodes] Thomas denominators (S4)
+    const ProblemConst* pc;
+    double* scratch;      // [B][nodes]
+};
+
+struct RhsModesArgs {
+    double* R;
+    uint64_t N;
+    int nodes, B, nmodes, scheme, rhs_mode;
+    double h, tau;
+    const double* a;      // [B][nmodes]
+    const double* k;      // [nmodes]
+    const double* p;      // [B][nmodes]
+    const int* trig;      // [nmodes]
+    const double* u0amp;  // [B] or null
+    const double* phiamp; // [B] or null
+    const double* wts;    // [B][N+1]: g (S4/ODE) or m (S3) weights
+    const double* cvals;  // [B] c (S3/S4) or mu (ODE)
+};
+
+
+struct SpecArgs;
+size_t mp_smem_bytes(int G, int m);
+cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st);
+cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
+                           cplx* spec, const cplx* tw, int logT, cudaStream_t st);
+cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
+                        int threads, cudaStream_t st);
+cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
+cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
+
+}  // namespace ftb
