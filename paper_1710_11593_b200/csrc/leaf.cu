@@ -245,9 +245,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
                     x[v] = fma(EL, lamq[v], Fv[v]);
             }
         }
-        // in-leaf history: push x into the remaining steps of the leaf
+        // in-leaf history: push x into the remaining steps of the leaf (padding
+        // nodes beyond the slab stay exactly zero)
 #pragma unroll
         for (int v = 0; v < NPT; ++v) {
+            if (tid * NPT + v >= mreal) x[v] = 0.0;
             tile[v][k] = x[v];
 #pragma unroll
             for (int k2 = k + 1; k2 < L; ++k2) tile[v][k2] = fma(-cw[k2 - k], x[v], tile[v][k2]);

@@ -110,8 +110,7 @@ __global__ void __launch_bounds__(kMpThreads) mp_kernel(MpArgs a) {
         if (tp < a.J - 1) {  // exact near field: lags t - j < J
             const double* cp = a.col + (uint64_t)pb * N;
             const double* x1 = a.X + row1 * N;
-            uint64_t jlo = t - (uint64_t)(a.J - 1);
-            if (jlo < a.lo) jlo = a.lo;
+            const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
             double s1 = 0.0, s2 = 0.0;
             for (uint64_t j = a.mid; j-- > jlo;) {
                 const double cv = cp[t - j];
