@@ -140,6 +140,21 @@ int ft_assemble_rhs_modes(const ft_plan* plan, int nmodes, const double* a, cons
 int ft_solve_fast(ft_plan* plan, const double* rhs, double* u, ft_report* report);
 int ft_solve_direct(ft_plan* plan, const double* rhs, double* u, ft_report* report);
 
+/* Diagnostics: one fast solve (device buffers only) with a CUDA event
+ * between every launch; per-launch device times for roofline accounting.
+ * kind 0 = leaf, 1 = history product (level = D&C level, n = 2L << level);
+ * first/len give the time range written, rows the rows touched. */
+typedef struct ft_op_time {
+    int kind;
+    int level;
+    uint64_t t0;
+    uint64_t len;
+    uint64_t bytes;  /* algorithmic HBM bytes of the launch */
+    float ms;
+} ft_op_time;
+int ft_profile_fast(ft_plan* plan, const double* rhs_device, double* u_device, ft_op_time* out,
+                    uint64_t capacity, uint64_t* count);
+
 int ft_set_stream(ft_plan* plan, void* cuda_stream);
 const char* ft_last_error(void);
 void ft_destroy(ft_plan* plan);

@@ -72,6 +72,11 @@ class _Report(C.Structure):
                 ("kernel_launches", C.c_uint64)]
 
 
+class _OpTime(C.Structure):
+    _fields_ = [("kind", C.c_int), ("level", C.c_int), ("t0", C.c_uint64), ("len", C.c_uint64),
+                ("bytes", C.c_uint64), ("ms", C.c_float)]
+
+
 class _Info(C.Structure):
     _fields_ = [("problems", C.c_uint64), ("nodes", C.c_uint64), ("time_steps", C.c_uint64),
                 ("leaf", C.c_uint64), ("levels", C.c_uint64), ("slabs", C.c_uint64),
@@ -85,7 +90,7 @@ _lib = None
 
 ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
-               "ft_set_stream", "ft_last_error", "ft_destroy")
+               "ft_profile_fast", "ft_set_stream", "ft_last_error", "ft_destroy")
 
 
 def lib() -> C.CDLL:
@@ -106,6 +111,7 @@ def lib() -> C.CDLL:
         L.ft_solve_fast.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_set_stream.argtypes = [P, P]
+        L.ft_profile_fast.argtypes = [P, P, P, C.POINTER(_OpTime), U64, C.POINTER(U64)]
         L.ft_last_error.restype = C.c_char_p
         L.ft_destroy.argtypes = [P]
         L.ft_destroy.restype = None
@@ -270,6 +276,19 @@ class Plan:
         report = SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
                              rep.device_ms, rep.kernel_launches)
         return out, report
+
+    def set_stream(self, stream_handle: int) -> None:
+        """Run on a caller's CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        _check(lib().ft_set_stream(self._h, stream_handle))
+
+    def profile_fast(self, rhs, out):
+        """Per-launch device times of one fast solve (device buffers)."""
+        cap = 4 * (self.N // 8 + 16)
+        arr = (_OpTime * cap)()
+        cnt = C.c_uint64(0)
+        _check(lib().ft_profile_fast(self._h, _ptr(rhs), _ptr(out), arr, cap, C.byref(cnt)))
+        return [dict(kind=arr[i].kind, level=arr[i].level, t0=arr[i].t0, len=arr[i].len,
+                     bytes=arr[i].bytes, ms=arr[i].ms) for i in range(min(cnt.value, cap))]
 
     def solve_fast(self, rhs, out=None):
         return self._solve(lib().ft_solve_fast, rhs, out)

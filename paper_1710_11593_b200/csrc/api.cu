@@ -81,8 +81,11 @@ struct ft_plan {
     int lp_stride = 0;
     cplx* tw_d = nullptr;
     cplx* spec_d = nullptr;
-    double* xch_d = nullptr;
-    unsigned* flags_d = nullptr;
+    double* xch_d = nullptr;      // multi-slab carries of the current leaf
+    double* kcoef_d = nullptr;    // single-CTA Dirichlet coefficients
+    double* respg_d = nullptr;    // multi-slab space-time response tables
+    double* resph_d = nullptr;
+    std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
     double* dw_d = nullptr;       // direct weights [B][N]
     double* cprime_d = nullptr;   // [B][nodes]
     double* den_d = nullptr;
@@ -135,14 +138,16 @@ void scan_params(ft_plan* p, int b, std::vector<double>& lampow) {
         lam = expl(-phi);
         const long double one_m = -expm1l(-phi);
         pc.lam = (double)lam;
-        pc.G0 = (double)(lam / (bb * one_m * (1.0L + lam)));
+        p->G0L[b] = lam / (bb * one_m * (1.0L + lam));
+        pc.G0 = (double)p->G0L[b];
         const long double Lam = expl(-phi * (long double)(p->nodes + 1));
         pc.Lam = (double)Lam;
         pc.inv1mL2 = (double)(1.0L / (1.0L - Lam * Lam));
     } else if (p->kind == SK_UPWIND) {
         lam = (long double)pc.off / (long double)pc.d;
         pc.lam = (double)lam;
-        pc.G0 = (double)(1.0L / (long double)pc.d);
+        p->G0L[b] = 1.0L / (long double)pc.d;
+        pc.G0 = (double)p->G0L[b];
         pc.Lam = 0.0;
         pc.inv1mL2 = 1.0;
     } else {
@@ -151,6 +156,7 @@ void scan_params(ft_plan* p, int b, std::vector<double>& lampow) {
         pc.Lam = 0.0;
         pc.inv1mL2 = 1.0;
     }
+    p->lamL[b] = lam;
     double* lp = lampow.data() + (uint64_t)b * p->lp_stride;
     for (int k = 0; k < p->lp_stride; ++k) {
         long double v;
@@ -158,6 +164,73 @@ void scan_params(ft_plan* p, int b, std::vector<double>& lampow) {
         else if (p->kind == SK_UPWIND) v = powl(lam, (long double)k);
         else v = k == 0 ? 1.0L : 0.0L;
         lp[k] = (double)v;
+    }
+}
+
+// Single-CTA Dirichlet correction  x_i += kF_i F_M + kB_i B_1  (i = q+1):
+// alpha lam^i + gam lam^(n+1-i) with alpha, gam from p0 = G0 lam B_1, pM1 = G0 lam F_M.
+void dirichlet_coefs(const ft_plan* p, int b, double* kF, double* kB) {
+    const int n = p->nodes;
+    const long double lam = p->lamL[b], G0 = p->G0L[b];
+    const long double phi = -logl(lam);
+    const long double Lam = expl(-phi * (long double)(n + 1));
+    const long double inv = 1.0L / (1.0L - Lam * Lam);
+    for (int q = 0; q < n; ++q) {
+        const long double li = expl(-phi * (long double)(q + 1));
+        const long double lr = expl(-phi * (long double)(n - q));
+        kF[q] = (double)(G0 * lam * inv * (Lam * li - lr));
+        kB[q] = (double)(G0 * lam * inv * (Lam * lr - li));
+    }
+}
+
+// Zero-carry local solve of one slab (long double) -> x, exported carries.
+void local_solve_ld(const ft_plan* p, int b, const std::vector<long double>& r, std::vector<long double>& x,
+                    long double& cF, long double& cB) {
+    const int ms = (int)r.size();
+    const long double lam = p->lamL[b], G0 = p->G0L[b];
+    std::vector<long double> F(ms), Bk(ms);
+    long double acc = 0.0L;
+    const bool tri = p->kind == SK_TRIDIAG;
+    for (int q = 0; q < ms; ++q) {
+        acc = lam * acc + (tri ? r[q] : r[q] * G0);  // upwind: G0 = 1/d
+        F[q] = acc;
+    }
+    acc = 0.0L;
+    for (int q = ms - 1; q >= 0; --q) {
+        acc = lam * acc + r[q];
+        Bk[q] = acc;
+    }
+    x.resize(ms);
+    for (int q = 0; q < ms; ++q) x[q] = tri ? G0 * (F[q] + Bk[q] - r[q]) : F[q];
+    cF = F[ms - 1];
+    cB = Bk[0];
+}
+
+// Space-time responses of a slab of ms nodes to unit left / right injections
+// (shapes lam^q, lam^(ms-1-q)) at lag 0: GL, GR [ms][L]; carry responses
+// h = (hFL, hFR, hBL, hBR)[L] (lag 0 entries are zero).
+void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][m][L]*/, double* H /*[L][4]*/) {
+    const int L = p->L, m = p->slab;
+    const double* col = p->col_h.data() + (uint64_t)b * p->N;
+    const long double lam = p->lamL[b];
+    for (int side = 0; side < 2; ++side) {
+        std::vector<std::vector<long double>> g(L, std::vector<long double>(ms));
+        for (int q = 0; q < ms; ++q) g[0][q] = powl(lam, (long double)(side == 0 ? q : ms - 1 - q));
+        H[0 * 4 + side] = 0.0;
+        H[0 * 4 + 2 + side] = 0.0;
+        for (int l = 1; l < L; ++l) {
+            std::vector<long double> dr(ms, 0.0L);
+            for (int lp = 0; lp < l; ++lp) {
+                const long double c = (uint64_t)(l - lp) < p->N ? (long double)col[l - lp] : 0.0L;
+                for (int q = 0; q < ms; ++q) dr[q] -= c * g[lp][q];
+            }
+            long double cF, cB;
+            local_solve_ld(p, b, dr, g[l], cF, cB);
+            H[l * 4 + side] = (double)cF;
+            H[l * 4 + 2 + side] = (double)cB;
+        }
+        for (int q = 0; q < m; ++q)
+            for (int l = 0; l < L; ++l) G[((uint64_t)side * m + q) * L + l] = q < ms ? (double)g[l][q] : 0.0;
     }
 }
 
@@ -171,7 +244,7 @@ void build_schedule(ft_plan* p) {
     for (uint64_t n = 2 * L; n <= Npad; n <<= 1) {
         Level lv;
         lv.n = (int)n;
-        lv.K = n <= 16384 ? 2 : (int)(n / 8192);
+        lv.K = n <= 2 * (uint64_t)kMpTile ? 2 : (int)(n / kMpTile);
         lv.m = (int)(n / lv.K);
         lv.G = lv.m >= kMpTile ? 1 : kMpTile / lv.m;
         if (lv.G > pairs) lv.G = pairs;
@@ -343,6 +416,8 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     }
     p->lp_stride = std::max(nodes + 2, 4098);
     std::vector<double> lampow((uint64_t)count * p->lp_stride);
+    p->lamL.assign(count, 0.0L);
+    p->G0L.assign(count, 0.0L);
     for (uint64_t b = 0; b < count; ++b) scan_params(p, (int)b, lampow);
     build_schedule(p);
 
@@ -360,19 +435,34 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     }
     if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * B * nodes))) return rc;
     if (p->multi) {
-        if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 4 * B * p->P))) return rc;
-        if ((rc = alloc_copy((void**)&p->flags_d, nullptr, sizeof(unsigned) * B * p->P))) return rc;
+        if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
+        const uint64_t gsz = (uint64_t)2 * 2 * p->slab * p->L, hsz = (uint64_t)2 * p->L * 4;
+        std::vector<double> G(B * gsz, 0.0), H(B * hsz, 0.0);
+        const int mlast = nodes - (p->P - 1) * p->slab;
+        for (uint64_t b = 0; b < B; ++b) {
+            slab_responses(p, (int)b, p->slab, G.data() + b * gsz, H.data() + b * hsz);
+            slab_responses(p, (int)b, mlast, G.data() + b * gsz + gsz / 2, H.data() + b * hsz + hsz / 2);
+        }
+        if ((rc = alloc_copy((void**)&p->respg_d, G.data(), sizeof(double) * G.size()))) return rc;
+        if ((rc = alloc_copy((void**)&p->resph_d, H.data(), sizeof(double) * H.size()))) return rc;
+    } else if (p->kind == SK_TRIDIAG) {
+        std::vector<double> kc(B * 2 * nodes);
+        for (uint64_t b = 0; b < B; ++b)
+            dirichlet_coefs(p, (int)b, kc.data() + b * 2 * nodes, kc.data() + b * 2 * nodes + nodes);
+        if ((rc = alloc_copy((void**)&p->kcoef_d, kc.data(), sizeof(double) * kc.size()))) return rc;
     }
-    // twiddles exp(-2 pi i k / T), long double
+    // multi-resolution twiddles tw[S + k] = exp(-2 pi i k / S), S = 1, 2, 4, ..., T (long double)
     {
         const uint64_t T = 1ull << p->logT;
-        std::vector<cplx> tw(T);
+        std::vector<cplx> tw(2 * T);
         const long double pi = 3.141592653589793238462643383279502884L;
-        for (uint64_t k = 0; k < T; ++k) {
-            const long double ang = 2.0L * pi * (long double)k / (long double)T;
-            tw[k] = {(double)cosl(ang), (double)(-sinl(ang))};
-        }
-        if ((rc = alloc_copy((void**)&p->tw_d, tw.data(), sizeof(cplx) * T))) return rc;
+        tw[0] = {1.0, 0.0};
+        for (uint64_t S = 1; S <= T; S <<= 1)
+            for (uint64_t k = 0; k < S; ++k) {
+                const long double ang = 2.0L * pi * (long double)k / (long double)S;
+                tw[S + k] = {(double)cosl(ang), (double)(-sinl(ang))};
+            }
+        if ((rc = alloc_copy((void**)&p->tw_d, tw.data(), sizeof(cplx) * 2 * T))) return rc;
     }
     FT_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     p->own_stream = true;
@@ -391,13 +481,14 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     return FT_OK;
 }
 
-int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches) {
+int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
+             std::vector<cudaEvent_t>* evs = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
-    if (p->multi) FT_CUDA(cudaMemsetAsync(p->flags_d, 0, sizeof(unsigned) * p->B * p->P, st));
-    unsigned step_base = 0;
     uint64_t nl = 0;
-    for (const Op& op : p->ops) {
+    for (size_t oi = 0; oi < p->ops.size(); ++oi) {
+        const Op& op = p->ops[oi];
+        if (evs) FT_CUDA(cudaEventRecord((*evs)[oi], st));
         if (op.kind == OP_LEAF) {
             LeafArgs a;
             a.X = X;
@@ -412,11 +503,11 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches) {
             a.col = p->col_d;
             a.lampow = p->lampow_d;
             a.lp_stride = p->lp_stride;
+            a.kcoef = p->kcoef_d;
             a.xch = p->xch_d;
-            a.flags = p->flags_d;
-            a.step_base = step_base;
+            a.resp_g = p->respg_d;
+            a.resp_h = p->resph_d;
             FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P, p->threads, st));
-            step_base += (unsigned)op.len;
         } else {
             const Level& lv = p->levels[op.level];
             MpArgs a;
@@ -442,6 +533,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches) {
         }
         ++nl;
     }
+    if (evs) FT_CUDA(cudaEventRecord(evs->back(), st));
     if (launches) *launches = nl;
     return FT_OK;
 }
@@ -670,11 +762,52 @@ int ft_solve_direct(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
     return solve_common(p, rhs, u, rep, false);
 }
 
+int ft_profile_fast(ft_plan* p, const double* rhs, double* u, ft_op_time* out, uint64_t cap,
+                    uint64_t* count) {
+    if (!p || !rhs || !u || !count) return set_err(FT_EINVAL, "ft_profile_fast: null argument");
+    if (!is_device_ptr(rhs) || !is_device_ptr(u))
+        return set_err(FT_EINVAL, "ft_profile_fast: device buffers expected");
+    FT_CUDA(cudaSetDevice(p->device));
+    std::vector<cudaEvent_t> evs(p->ops.size() + 1);
+    for (auto& e : evs) FT_CUDA(cudaEventCreate(&e));
+    uint64_t nl = 0;
+    int rc = run_fast(p, u, rhs, &nl, &evs);
+    if (rc) return rc;
+    FT_CUDA(cudaStreamSynchronize(p->stream));
+    const uint64_t rows = rows_of(p);
+    const uint64_t n_ops = p->ops.size();
+    for (uint64_t i = 0; i < n_ops && i < cap; ++i) {
+        const Op& op = p->ops[i];
+        ft_op_time& o = out[i];
+        float ms = 0.f;
+        FT_CUDA(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
+        o.ms = ms;
+        if (op.kind == OP_LEAF) {
+            o.kind = 0;
+            o.level = -1;
+            o.t0 = op.t0;
+            o.len = (uint64_t)op.len;
+            o.bytes = 16ull * rows * o.len;  // read R, write U
+        } else {
+            const uint64_t h = op.mid - op.t0;
+            const uint64_t tend = std::min<uint64_t>(op.hi, p->N);
+            o.kind = 1;
+            o.level = op.level;
+            o.t0 = op.mid;
+            o.len = tend - op.mid;
+            o.bytes = 8ull * rows * h + 16ull * rows * o.len;  // read U half, read+write R half
+        }
+    }
+    *count = n_ops;
+    for (auto& e : evs) cudaEventDestroy(e);
+    return FT_OK;
+}
+
 void ft_destroy(ft_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->flags_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev0) cudaEventDestroy(p->ev0);

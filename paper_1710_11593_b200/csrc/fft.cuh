@@ -82,23 +82,49 @@ __device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
     for (int q = 0; q < R; ++q) v[q] = t[q];
 }
 
+// Twiddles w_S^(j q), q = 1..R-1, from the multi-resolution table
+// tw[S' + k] = exp(-2 pi i k / S') (every power-of-two S'): four coalesced loads
+// (w_S^j, w_{S/2}^j = w_S^2j, w_{S/4}^j, w_{S/8}^j) and at most 11 products.
+template <int R>
+__device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restrict__ tw, int S, int j) {
+    w[0] = {1.0, 0.0};
+    if (R >= 2) w[1] = ldgc(&tw[S + j]);
+    if (R >= 4) {
+        w[2] = ldgc(&tw[(S >> 1) + j]);
+        w[3] = cmul(w[1], w[2]);
+    }
+    if (R >= 8) {
+        w[4] = ldgc(&tw[(S >> 2) + j]);
+#pragma unroll
+        for (int q = 5; q < 8; ++q) w[q] = cmul(w[4], w[q - 4]);
+    }
+    if (R >= 16) {
+        w[8] = ldgc(&tw[(S >> 3) + j]);
+#pragma unroll
+        for (int q = 9; q < 16; ++q) w[q] = cmul(w[8], w[q - 8]);
+    }
+}
+
 // One in-place DIF pass over all sequences of `total` points, group size S.
 template <int R>
 __device__ __forceinline__ void fwd_pass(cplx* buf, int total, int S, const cplx* __restrict__ tw,
                                          int logT, int logS) {
-    const int Q = S / R;
-    const int tasks = total / R;
+    constexpr int LR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    const int logQ = logS - LR;
+    const int Q = 1 << logQ;
+    const int tasks = total >> LR;
     for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
         const int j = t & (Q - 1);
-        const int base = (t / Q) * S + j;
+        const int base = ((t >> logQ) << logS) + j;
         cplx v[R];
 #pragma unroll
         for (int p = 0; p < R; ++p) v[p] = buf[sphys(base + p * Q)];
         dft_reg<R, false>(v);
         if (Q > 1) {
-            const int sh = logT - logS;
+            cplx w[R];
+            pass_twiddles<R>(w, tw, S, j);
 #pragma unroll
-            for (int q = 1; q < R; ++q) v[q] = cmul(v[q], ldgc(&tw[(j * q) << sh]));
+            for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
         }
 #pragma unroll
         for (int q = 0; q < R; ++q) buf[sphys(base + q * Q)] = v[q];
@@ -108,18 +134,21 @@ __device__ __forceinline__ void fwd_pass(cplx* buf, int total, int S, const cplx
 template <int R>
 __device__ __forceinline__ void inv_pass(cplx* buf, int total, int S, const cplx* __restrict__ tw,
                                          int logT, int logS) {
-    const int Q = S / R;
-    const int tasks = total / R;
+    constexpr int LR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    const int logQ = logS - LR;
+    const int Q = 1 << logQ;
+    const int tasks = total >> LR;
     for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
         const int j = t & (Q - 1);
-        const int base = (t / Q) * S + j;
+        const int base = ((t >> logQ) << logS) + j;
         cplx v[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) v[q] = buf[sphys(base + q * Q)];
         if (Q > 1) {
-            const int sh = logT - logS;
+            cplx w[R];
+            pass_twiddles<R>(w, tw, S, j);
 #pragma unroll
-            for (int q = 1; q < R; ++q) v[q] = cmulc(v[q], ldgc(&tw[(j * q) << sh]));
+            for (int q = 1; q < R; ++q) v[q] = cmulc(v[q], w[q]);
         }
         dft_reg<R, true>(v);
 #pragma unroll

@@ -28,8 +28,10 @@ struct ProblemConst {
 };
 
 constexpr int kLeafThreads = 256;
+constexpr int kMaxSlabs = 160;  // slabs per problem in the multi-slab leaf
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
+constexpr int kMpDirectMaxH = 128;  // blocks n <= 256 use the direct Toeplitz kernel
 
 struct __align__(16) cplx {
     double x, y;
@@ -63,9 +65,10 @@ struct LeafArgs {
     const double* col;         // [B][N] Toeplitz first columns
     const double* lampow;      // [B][lp_stride]: lam^k, k = 0..lp_stride-1
     int lp_stride;
-    double* xch;               // multi-slab exchange [2][B*P][2]
-    unsigned* flags;           // [B*P] step flags (multi-slab)
-    unsigned step_base;        // steps completed before this leaf in the current solve
+    const double* kcoef;       // [B][2][nodes] single-CTA Dirichlet coefficients kF, kB
+    double* xch;               // multi-slab carries of the current leaf [B*P][L][2]
+    const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
+    const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
 };
 
 struct MpArgs {
@@ -113,6 +116,7 @@ struct RhsModesArgs {
 
 struct SpecArgs;
 size_t mp_smem_bytes(int G, int m);
+bool mp_is_direct(int n);
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st);
 cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
                            cplx* spec, const cplx* tw, int logT, cudaStream_t st);

@@ -1,38 +1,134 @@
 // leaf.cu -- the leaf of the time-axis divide-and-conquer: L consecutive time
-// steps, each one a spatial solve of the step operator, with the in-leaf
-// history (lags < L) applied exactly in registers.
+// steps, each a spatial solve of the step operator, with the in-leaf history
+// (lags < L) applied exactly in registers.
 //
 // Step operator solve: instead of the reference's Thomas
-// sweep (src/schemes.cpp:453-461), which is sequential over nodes and loses
-// ~1e-10 relative on the cfg4 operator, the constant tridiagonal operator
+// sweep (src/schemes.cpp:453-461), sequential over nodes and ~1e-10 relative
+// off on the cfg4 operator, the constant tridiagonal operator
 // d I - b (S + S^T) with Dirichlet ends is inverted through its Green's
-// function:  x = G0 (F + B - r) + alpha lam^i + gam lam^(n+1-i)  where F and B
-// are forward / backward lam-decay scans of r.  Scans are parallel (thread,
-// warp shuffle, cross-warp) and accurate to ~1e-13 on cfg4 (probe in DESIGN.md).
-// The upwind operator of Scheme 3 (src/schemes.cpp:345-351) is the forward
-// scan alone; the ODE is a scalar divide.
+// function   x = G0 (F + B - r) + alpha lam^i + gam lam^(n+1-i)   where F and B
+// are forward / backward lam-decay scans of r (thread, warp shuffle,
+// cross-warp).  The upwind operator of Scheme 3 (src/schemes.cpp:345-351) is the
+// forward scan alone; the ODE is a scalar divide.
 //
-// Multi-slab mode (problems larger than one CTA): each CTA owns a contiguous
-// slab of nodes and publishes two scan carries per step; every CTA combines
-// the carries of all slabs of its problem (cooperative launch, per-step flags).
+// Problems wider than one CTA are split into slabs (one CTA each) and solved
+// in three phases per leaf, with ONE cross-CTA exchange per leaf instead of
+// one per step (space-time SPIKE):
+//   1 (leaf_kernel<..., LOCAL>) every slab marches L steps with zero
+//     inter-slab carries, recording the two carries it would export per step;
+//   2 (leaf_correct) every CTA replays the small reduced recursion over all
+//     slabs' carries (lag responses h*), giving its own slab's injections
+//     EL_k, ER_k;
+//   3 (leaf_correct) the slab's solution is corrected with precomputed
+//     space-time response tables GL, GR: x += sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l).
 #include "internal.cuh"
 
 namespace ftb {
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+template <int NPT>
+struct ScanConsts {
+    double lam;
+    double pwF[5], pwB[5];  // masked lane multipliers lam^(NPT 2^d) (0 where the partner is out of range)
+    double lamv1[NPT], lamNv[NPT];
+    double lamLaneF, lamLaneB, lamW;  // lam^(NPT lane), lam^(NPT (31-lane)), lam^(32 NPT)
+    double exFmask, exBmask;
+};
+
+template <int NPT>
+__device__ __forceinline__ void scan_consts(ScanConsts<NPT>& sc, const double* lp, int lp_stride, double lam,
+                                            int lane) {
+    sc.lam = lam;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const double p = lp[min(NPT << d, lp_stride - 1)];
+        sc.pwF[d] = lane >= (1 << d) ? p : 0.0;
+        sc.pwB[d] = lane + (1 << d) < 32 ? p : 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v < NPT; ++v) {
+        sc.lamv1[v] = lp[v + 1];
+        sc.lamNv[v] = lp[NPT - v];
+    }
+    sc.lamLaneF = lp[min(NPT * lane, lp_stride - 1)];
+    sc.lamLaneB = lp[min(NPT * (31 - lane), lp_stride - 1)];
+    sc.lamW = lp[min(32 * NPT, lp_stride - 1)];
+    sc.exFmask = lane > 0 ? 1.0 : 0.0;
+    sc.exBmask = lane < 31 ? 1.0 : 0.0;
 }
 
-template <int KIND, int NPT, int L, bool MULTI>
+// Forward (and, for TRIDIAG, backward) lam-decay scans over the CTA's nodes
+// with zero carry in at both ends.  Fv/Bv: scans at this thread's nodes;
+// totF: F at the CTA's last (possibly padding) node; totB: B at its first.
+template <int KIND, int NPT>
+__device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanConsts<NPT>& sc,
+                                         double (*s_wt)[2], int lane, int w, int nw, double (&Fv)[NPT],
+                                         double (&Bv)[NPT], double& totF, double& totB) {
+    constexpr bool TRI = KIND == SK_TRIDIAG;
+    double f[NPT], bl[NPT];
+    double acc = 0.0;
+#pragma unroll
+    for (int v = 0; v < NPT; ++v) {
+        acc = fma(sc.lam, acc, in[v]);
+        f[v] = acc;
+    }
+    double SF = acc, SB = 0.0;
+    if (TRI) {
+        double accb = 0.0;
+#pragma unroll
+        for (int v = NPT - 1; v >= 0; --v) {
+            accb = fma(sc.lam, accb, in[v]);
+            bl[v] = accb;
+        }
+        SB = accb;
+    }
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const double yF = __shfl_up_sync(0xffffffffu, SF, 1 << d);
+        SF = fma(sc.pwF[d], yF, SF);
+        if (TRI) {
+            const double yB = __shfl_down_sync(0xffffffffu, SB, 1 << d);
+            SB = fma(sc.pwB[d], yB, SB);
+        }
+    }
+    const double exF = sc.exFmask * __shfl_up_sync(0xffffffffu, SF, 1);
+    const double exB = TRI ? sc.exBmask * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
+    if (lane == 31) s_wt[w][0] = SF;
+    if (lane == 0) s_wt[w][1] = SB;
+    __syncthreads();
+    // cross-warp carries: short sequential chains over the (<= 8) warp totals
+    double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
+#pragma unroll 8
+    for (int ww = 0; ww < nw; ++ww) {
+        if (ww == w) CF = runF;
+        runF = fma(sc.lamW, runF, s_wt[ww][0]);
+        if (TRI) {
+            const int wb = nw - 1 - ww;
+            if (wb == w) CB = runB;
+            runB = fma(sc.lamW, runB, s_wt[wb][1]);
+        }
+    }
+    totF = runF;
+    totB = runB;
+    const double Fprev = fma(sc.lamLaneF, CF, exF);
+#pragma unroll
+    for (int v = 0; v < NPT; ++v) Fv[v] = fma(sc.lamv1[v], Fprev, f[v]);
+    if (TRI) {
+        const double Bnext = fma(sc.lamLaneB, CB, exB);
+#pragma unroll
+        for (int v = 0; v < NPT; ++v) Bv[v] = fma(sc.lamNv[v], Bnext, bl[v]);
+    }
+}
+
+// MODE 0 (SINGLE): the CTA spans the whole problem; the Dirichlet correction
+//   x += kF_i F_M + kB_i B_1 (host-precomputed per node) makes the step exact.
+// MODE 1 (LOCAL): phase 1 of the slab decomposition (zero inter-slab carries);
+//   per step the slab's exported carries (F at its last node, B at its first)
+//   are written to xch[cta][k][2].
+template <int KIND, int NPT, int L, int MODE>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
-    __shared__ double s_wt[2][32][2];  // per-warp scan totals (double buffered)
-    __shared__ double s_own[2][2];     // padded-slab owner values (F at last node, B at first)
-    __shared__ double s_ext[2][2];     // multi-slab EL / ER
+    __shared__ double s_wt[2][32][2];
+    __shared__ double s_own[2];
+    __shared__ double s_cx[L][2];
 
     const int cta = blockIdx.x;
     const int pb = cta / a.P, s = cta - pb * a.P;
@@ -60,33 +156,18 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
         for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? src[k] : 0.0;
     }
-
-    // decay powers
-    const double lam = pc.lam;
-    double lamq[NPT], lamR[NPT], lamv1[NPT], lamNv[NPT];
+    ScanConsts<NPT> sc;
+    scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);
+    // Dirichlet correction coefficients (SINGLE mode)
+    double kF[NPT], kB[NPT];
 #pragma unroll
     for (int v = 0; v < NPT; ++v) {
         const int q = tid * NPT + v;
-        lamq[v] = lp[min(q, a.lp_stride - 1)];
-        lamR[v] = (q < mreal) ? lp[mreal - 1 - q] : 0.0;
-        lamv1[v] = lp[v + 1];
-        lamNv[v] = lp[NPT - v];
+        const bool valid = q < mreal;
+        kF[v] = (MODE == 0 && KIND == SK_TRIDIAG && valid) ? a.kcoef[(uint64_t)pb * 2 * a.nodes + q] : 0.0;
+        kB[v] = (MODE == 0 && KIND == SK_TRIDIAG && valid) ? a.kcoef[(uint64_t)pb * 2 * a.nodes + a.nodes + q] : 0.0;
     }
-    double pw[5], pwW[5];
-#pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        pw[d] = lp[min(NPT << d, a.lp_stride - 1)];
-        pwW[d] = lp[min((32 * NPT) << d, a.lp_stride - 1)];
-    }
-    const double lamLaneF = lp[min(NPT * lane, a.lp_stride - 1)];
-    const double lamLaneB = lp[min(NPT * (31 - lane), a.lp_stride - 1)];
-
-    // owner of the last real node of the slab
     const int own_t = (mreal - 1) / NPT, own_v = (mreal - 1) - own_t * NPT;
-
-    // multi-slab constants
-    const double lamA = MULTI ? lp[min(slab0 + 1, a.lp_stride - 1)] : lam;                   // lam^(a_s)
-    const double lamB = MULTI ? lp[min(a.nodes - (slab0 + mreal) + 1, a.lp_stride - 1)] : lam;  // lam^(n+1-b_s)
 
 #pragma unroll
     for (int k = 0; k < L; ++k) {
@@ -97,152 +178,33 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
             for (int v = 0; v < NPT; ++v) x[v] = tile[v][k] / pc.d;
         } else {
-            // ---- forward scan (both kinds) ----
             double in[NPT];
 #pragma unroll
             for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][k] / pc.d : tile[v][k];
-            double f[NPT];
-            double acc = 0.0;
-#pragma unroll
-            for (int v = 0; v < NPT; ++v) {
-                acc = fma(lam, acc, in[v]);
-                f[v] = acc;
-            }
-            double SF = acc;
-#pragma unroll
-            for (int d = 0; d < 5; ++d) {
-                const double y = __shfl_up_sync(0xffffffffu, SF, 1 << d);
-                if (lane >= (1 << d)) SF = fma(pw[d], y, SF);
-            }
-            double exF = __shfl_up_sync(0xffffffffu, SF, 1);
-            if (lane == 0) exF = 0.0;
-            // ---- backward scan (tridiagonal only) ----
-            double bl[NPT];
-            double SB = 0.0, exB = 0.0;
-            if (KIND == SK_TRIDIAG) {
-                double accb = 0.0;
-#pragma unroll
-                for (int v = NPT - 1; v >= 0; --v) {
-                    accb = fma(lam, accb, in[v]);
-                    bl[v] = accb;
-                }
-                SB = accb;
-#pragma unroll
-                for (int d = 0; d < 5; ++d) {
-                    const double y = __shfl_down_sync(0xffffffffu, SB, 1 << d);
-                    if (lane + (1 << d) < 32) SB = fma(pw[d], y, SB);
-                }
-                exB = __shfl_down_sync(0xffffffffu, SB, 1);
-                if (lane == 31) exB = 0.0;
-            }
-            if (lane == 31) s_wt[par][w][0] = SF;
-            if (lane == 0) s_wt[par][w][1] = SB;
-            __syncthreads();
-            // ---- cross-warp carries (every warp redundantly) ----
-            double tf = lane < nw ? s_wt[par][lane][0] : 0.0;
-            double tb = lane < nw ? s_wt[par][lane][1] : 0.0;
-#pragma unroll
-            for (int d = 0; d < 5; ++d) {
-                const double y = __shfl_up_sync(0xffffffffu, tf, 1 << d);
-                if (lane >= (1 << d)) tf = fma(pwW[d], y, tf);
-                if (KIND == SK_TRIDIAG) {
-                    const double z = __shfl_down_sync(0xffffffffu, tb, 1 << d);
-                    if (lane + (1 << d) < nw) tb = fma(pwW[d], z, tb);
-                }
-            }
-            const double CF = w > 0 ? __shfl_sync(0xffffffffu, tf, w - 1) : 0.0;  // F at last node of warp w-1
-            const double totF = __shfl_sync(0xffffffffu, tf, nw - 1);             // F at padded end
-            double CB = 0.0, totB = 0.0;
-            if (KIND == SK_TRIDIAG) {
-                CB = (w + 1 < nw) ? __shfl_sync(0xffffffffu, tb, w + 1) : 0.0;
-                totB = __shfl_sync(0xffffffffu, tb, 0);
-            }
-            const double Fprev = fma(lamLaneF, CF, exF);
-            double Fv[NPT], Bv[NPT];
-#pragma unroll
-            for (int v = 0; v < NPT; ++v) Fv[v] = fma(lamv1[v], Fprev, f[v]);
-            if (KIND == SK_TRIDIAG) {
-                const double Bnext = fma(lamLaneB, CB, exB);
-#pragma unroll
-                for (int v = 0; v < NPT; ++v) Bv[v] = fma(lamNv[v], Bnext, bl[v]);
-            }
-            // slab totals: F at the last real node, B at the first node
-            double cF = totF, cB = totB;
-            if (padded) {
+            double Fv[NPT], Bv[NPT], totF, totB;
+            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, nw, Fv, Bv, totF, totB);
+            double cF = totF;
+            if (padded) {  // F at the last real node (padding nodes carry zeros)
                 if (tid == own_t) {
 #pragma unroll
                     for (int v = 0; v < NPT; ++v)
-                        if (v == own_v) s_own[par][0] = Fv[v];
+                        if (v == own_v) s_own[par] = Fv[v];
                 }
                 __syncthreads();
-                cF = s_own[par][0];
+                cF = s_own[par];
             }
-            double EL = 0.0, ER = 0.0;
-            if (!MULTI) {
-                if (KIND == SK_TRIDIAG) {
-                    const double p0 = pc.G0 * lam * cB, pM1 = pc.G0 * lam * cF;
-                    const double alpha = (pc.Lam * pM1 - p0) * pc.inv1mL2;
-                    const double gam = (pc.Lam * p0 - pM1) * pc.inv1mL2;
-                    EL = alpha * lam;
-                    ER = gam * lam;
-                }
-            } else {
-                // publish this slab's carries, gather every slab's
-                const unsigned stepno = a.step_base + (unsigned)k + 1u;
-                double* xch = a.xch + (uint64_t)par * gridDim.x * 2;
-                if (tid == 0) {
-                    xch[2 * cta] = cF;
-                    xch[2 * cta + 1] = cB;
-                    __threadfence();
-                    st_release(&a.flags[cta], stepno);
-                }
-                if (w == 0) {
-                    const int base = pb * a.P;
-                    double fin = 0.0, bin = 0.0, fM = 0.0, b1 = 0.0;
-                    for (int s2 = lane; s2 < a.P; s2 += 32) {
-                        while (ld_acquire(&a.flags[base + s2]) < stepno) {
-                        }
-                        const double f2 = __ldcg(&xch[2 * (base + s2)]);
-                        const double b2 = __ldcg(&xch[2 * (base + s2) + 1]);
-                        const int s0 = s2 * a.slab;
-                        const int last = min(s0 + a.slab, a.nodes) - 1;
-                        if (s2 < s) fin = fma(lp[slab0 - 1 - last], f2, fin);
-                        if (s2 > s) bin = fma(lp[s0 - (slab0 + mreal)], b2, bin);
-                        if (KIND == SK_TRIDIAG) {
-                            fM = fma(lp[a.nodes - 1 - last], f2, fM);
-                            b1 = fma(lp[s0], b2, b1);
-                        }
-                    }
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) {
-                        fin += __shfl_xor_sync(0xffffffffu, fin, o);
-                        bin += __shfl_xor_sync(0xffffffffu, bin, o);
-                        fM += __shfl_xor_sync(0xffffffffu, fM, o);
-                        b1 += __shfl_xor_sync(0xffffffffu, b1, o);
-                    }
-                    if (lane == 0) {
-                        if (KIND == SK_TRIDIAG) {
-                            const double p0 = pc.G0 * lam * b1, pM1 = pc.G0 * lam * fM;
-                            const double alpha = (pc.Lam * pM1 - p0) * pc.inv1mL2;
-                            const double gam = (pc.Lam * p0 - pM1) * pc.inv1mL2;
-                            s_ext[par][0] = pc.G0 * lam * fin + alpha * lamA;
-                            s_ext[par][1] = pc.G0 * lam * bin + gam * lamB;
-                        } else {
-                            s_ext[par][0] = lam * fin;
-                            s_ext[par][1] = 0.0;
-                        }
-                    }
-                }
-                __syncthreads();
-                EL = s_ext[par][0];
-                ER = s_ext[par][1];
+            if (MODE == 1 && tid == 0) {
+                s_cx[k][0] = cF;
+                s_cx[k][1] = totB;
             }
 #pragma unroll
             for (int v = 0; v < NPT; ++v) {
-                if (KIND == SK_TRIDIAG)
-                    x[v] = fma(pc.G0, Fv[v] + Bv[v] - tile[v][k], fma(EL, lamq[v], ER * lamR[v]));
-                else
-                    x[v] = fma(EL, lamq[v], Fv[v]);
+                if (KIND == SK_TRIDIAG) {
+                    const double base = pc.G0 * (Fv[v] + Bv[v] - in[v]);
+                    x[v] = MODE == 0 ? fma(kF[v], cF, fma(kB[v], totB, base)) : base;
+                } else {
+                    x[v] = Fv[v];
+                }
             }
         }
         // in-leaf history: push x into the remaining steps of the leaf (padding
@@ -266,28 +228,210 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
                 if (k < len) dst[k] = tile[v][k];
         }
     }
+    if (MODE == 1) {
+        __syncthreads();
+        double* xo = a.xch + (uint64_t)cta * L * 2;
+        for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
+    }
+}
+
+// Phase 2 + 3 of the slab decomposition (see file header).  One CTA per slab;
+// phase 2 runs on the first ceil(P/32) warps (one slab per lane) and is
+// replayed redundantly by every CTA (no second exchange).
+template <int KIND, int NPT, int L>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    double* s_c0 = s_dyn;                   // [P][L][2] phase-1 carries of every slab
+    __shared__ double s_h[2][L][4];         // lag responses (main slab, last slab): hFL hFR hBL hBR
+    __shared__ double s_inj[L][2];          // this slab's EL_k, ER_k
+    __shared__ double s_part[2][8][2];      // cross-warp scan partials (double buffered)
+    __shared__ double s_tot[2];             // F_M, B_1
+
+    constexpr bool TRI = KIND == SK_TRIDIAG;
+    const int cta = blockIdx.x;
+    const int pb = cta / a.P, s = cta - pb * a.P;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int P = a.P;
+    const int nw2 = (P + 31) >> 5;          // phase-2 warps
+    const ProblemConst pc = a.pc[pb];
+    const double lam = pc.lam;
+    const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
+    const int len = a.len;
+    const int m = a.slab;
+    const int mlast = a.nodes - (P - 1) * m;
+
+    // load the carries of every slab of this problem and the response tables
+    const double* xin = a.xch + (uint64_t)pb * P * L * 2;
+    for (int i = tid; i < P * L * 2; i += blockDim.x) s_c0[i] = __ldcg(&xin[i]);
+    const double* hsrc = a.resp_h + (uint64_t)pb * 2 * L * 4;
+    for (int i = tid; i < 2 * L * 4; i += blockDim.x) (&s_h[0][0][0])[i] = hsrc[i];
+    __syncthreads();
+
+    // ---- phase 2: reduced recursion (warps < nw2, lane <-> slab) ----
+    if (w < nw2) {
+        const int sl = w * 32 + lane;          // slab owned by this lane
+        const bool act = sl < P;
+        const int ht = (sl == P - 1) ? 1 : 0;  // response table of this slab
+        const double mu = lp[min(m, a.lp_stride - 1)];          // lam^m between slab ends
+        const double mu_last = lp[min(mlast, a.lp_stride - 1)];
+        double pw[5], pwb[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            const double p = lp[min(m << d, a.lp_stride - 1)];
+            pw[d] = lane >= (1 << d) ? p : 0.0;
+            pwb[d] = lane + (1 << d) < 32 ? p : 0.0;
+        }
+        const double muW = lp[min(32 * m, a.lp_stride - 1)];
+        const double exm = lane > 0 ? 1.0 : 0.0, exbm = lane < 31 ? 1.0 : 0.0;
+        const double lamA = act ? lp[min(sl * m + 1, a.lp_stride - 1)] : 0.0;
+        const int last_s = act ? min(sl * m + m, a.nodes) - 1 : 0;
+        const double lamB = act ? lp[min(a.nodes - last_s, a.lp_stride - 1)] : 0.0;
+        const double lmF = lp[min(m * lane, a.lp_stride - 1)];
+        const double lmB = lp[min(m * (31 - lane), a.lp_stride - 1)];
+        double ELh[L], ERh[L];
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            ELh[k] = 0.0;
+            ERh[k] = 0.0;
+        }
+        const int nth2 = nw2 * 32;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            if (k >= len) break;
+            double cF = act ? s_c0[(sl * L + k) * 2] : 0.0;
+            double cB = act ? s_c0[(sl * L + k) * 2 + 1] : 0.0;
+            double aF0 = 0.0, aF1 = 0.0, aB0 = 0.0, aB1 = 0.0;
+#pragma unroll
+            for (int l = 1; l <= k; ++l) {
+                const double* h = s_h[ht][l];
+                aF0 = fma(h[0], ELh[k - l], aF0);
+                aF1 = fma(h[1], ERh[k - l], aF1);
+                if (TRI) {
+                    aB0 = fma(h[2], ELh[k - l], aB0);
+                    aB1 = fma(h[3], ERh[k - l], aB1);
+                }
+            }
+            if (act) {
+                cF += aF0 + aF1;
+                cB += aB0 + aB1;
+            } else {
+                cF = 0.0;
+                cB = 0.0;
+            }
+            // inclusive scans over slabs (uniform multiplier lam^m)
+            double SF = cF, SB = cB;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                SF = fma(pw[d], __shfl_up_sync(0xffffffffu, SF, 1 << d), SF);
+                if (TRI) SB = fma(pwb[d], __shfl_down_sync(0xffffffffu, SB, 1 << d), SB);
+            }
+            const double exF = exm * __shfl_up_sync(0xffffffffu, SF, 1);
+            const double exB = TRI ? exbm * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
+            // double-buffered partials: one named barrier separates write and read
+            double (*part)[2] = s_part[k & 1];
+            if (lane == 31) part[w][0] = SF;
+            if (lane == 0) part[w][1] = SB;
+            asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
+            double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
+            for (int ww = 0; ww < nw2; ++ww) {
+                if (ww == w) CF = runF;
+                runF = fma(muW, runF, part[ww][0]);
+                if (TRI) {
+                    const int wb = nw2 - 1 - ww;
+                    if (wb == w) CB = runB;
+                    runB = fma(muW, runB, part[wb][1]);
+                }
+            }
+            // exclusive carries into this slab: F at the node before it, B after it
+            const double FLin = fma(lmF, CF, exF);
+            const double BRin = TRI ? fma(lmB, CB, exB) : 0.0;
+            double* tot = s_tot;
+            if (sl == P - 1) tot[0] = fma(mu_last, FLin, cF);  // F at node n-1
+            if (sl == 0) tot[1] = fma(mu, BRin, cB);            // B at node 0
+            asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
+            double EL, ER;
+            if (TRI) {
+                const double p0 = pc.G0 * lam * tot[1], pM1 = pc.G0 * lam * tot[0];
+                const double alpha = (pc.Lam * pM1 - p0) * pc.inv1mL2;
+                const double gam = (pc.Lam * p0 - pM1) * pc.inv1mL2;
+                EL = fma(pc.G0 * lam, FLin, alpha * lamA);
+                ER = fma(pc.G0 * lam, BRin, gam * lamB);
+            } else {
+                EL = lam * FLin;
+                ER = 0.0;
+            }
+            if (!act) {
+                EL = 0.0;
+                ER = 0.0;
+            }
+            ELh[k] = EL;
+            ERh[k] = ER;
+            if (sl == s) {
+                s_inj[k][0] = EL;
+                s_inj[k][1] = ER;
+            }
+            // s_tot / s_part are rewritten next step only after its first barrier,
+            // which every reader of this step has passed
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 3: x = x0 + sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l) ----
+    const int slab0 = s * m;
+    const int mreal = min(m, a.nodes - slab0);
+    const int tsel = (s == P - 1) ? 1 : 0;
+    const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
+    for (int q = tid; q < mreal; q += blockDim.x) {
+        double* xr = a.X + (uint64_t)(pb * a.nodes + slab0 + q) * a.N + a.t0;
+        const double* gl = GT + (uint64_t)q * L;
+        const double* gr = GT + (uint64_t)(m + q) * L;
+        double g1[L], g2[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            g1[l] = gl[l];
+            g2[l] = TRI ? gr[l] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            if (k >= len) break;
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int l = 0; l <= k; ++l) {
+                acc0 = fma(g1[l], s_inj[k - l][0], acc0);
+                if (TRI) acc1 = fma(g2[l], s_inj[k - l][1], acc1);
+            }
+            xr[k] += acc0 + acc1;
+        }
+    }
 }
 
 // ---- host launch -------------------------------------------------------------
 
-template <int KIND, int NPT, int L, bool MULTI>
-static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, cudaStream_t st) {
-    if (MULTI) {
-        void* args[] = {(void*)&a};
-        return cudaLaunchCooperativeKernel((const void*)leaf_kernel<KIND, NPT, L, MULTI>, dim3(ctas),
-                                           dim3(threads), args, 0, st);
+template <int KIND, int NPT, int L>
+static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool multi, cudaStream_t st) {
+    if (!multi) {
+        leaf_kernel<KIND, NPT, L, 0><<<ctas, threads, 0, st>>>(a);
+        return cudaGetLastError();
     }
-    leaf_kernel<KIND, NPT, L, MULTI><<<ctas, threads, 0, st>>>(a);
+    leaf_kernel<KIND, NPT, L, 1><<<ctas, threads, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(double) * (size_t)a.P * L * 2;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(leaf_correct<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxSlabs * L * 2 * (int)sizeof(double));
+        attr = true;
+    }
+    leaf_correct<KIND, NPT, L><<<ctas, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-// Supported (NPT, L) pairs: tile of NPT*L doubles per thread.
+// Supported (kind, NPT, L): register tile of NPT*L doubles per thread.
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
                         int threads, cudaStream_t st) {
-#define FTB_LEAF_CASE(K_, NPT_, L_)                                                      \
-    if (kind == K_ && npt == NPT_ && L == L_)                                             \
-        return multi ? launch_leaf_t<K_, NPT_, L_, true>(a, ctas, threads, st)            \
-                     : launch_leaf_t<K_, NPT_, L_, false>(a, ctas, threads, st);
+#define FTB_LEAF_CASE(K_, NPT_, L_) \
+    if (kind == K_ && npt == NPT_ && L == L_) return launch_leaf_t<K_, NPT_, L_>(a, ctas, threads, multi, st);
     FTB_LEAF_CASE(SK_DIAG, 1, 32)
     FTB_LEAF_CASE(SK_TRIDIAG, 1, 32)
     FTB_LEAF_CASE(SK_TRIDIAG, 2, 32)

@@ -27,41 +27,54 @@ namespace ftb {
 
 __device__ __forceinline__ cplx conjc(cplx a) { return {a.x, -a.y}; }
 
-__global__ void __launch_bounds__(kMpThreads) mp_kernel(MpArgs a) {
+struct PairInfo {
+    uint64_t row1;  // first row of the packed pair
+    int pb;         // problem index
+    int has2;       // second row exists
+};
+
+template <int K>
+__global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    __shared__ PairInfo s_pair[kMpTile / 32];
     cg::cluster_group cluster = cg::this_cluster();
     const int b = (int)cluster.block_rank();
-    const int K = a.K, m = a.m, G = a.G, n = a.n;
-    const int logm = __ffs(m) - 1, logn = __ffs(n) - 1, logK = __ffs(K) - 1;
-    const int shT_n = a.logT - logn, shT_K = a.logT - logK;
+    const int m = a.m, G = a.G, n = a.n;
+    const int logm = __ffs(m) - 1;
     const int total = G * m;
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
     const int pair0 = blockIdx.y * G;
     const uint64_t N = a.N;
 
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int rp = min(pair0 + g, npairs - 1);
+        const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+        const int i1 = 2 * lp;
+        s_pair[g] = {(uint64_t)(pb * a.nodes + i1), pb, (pair0 + g < npairs && i1 + 1 < a.nodes) ? 1 : 0};
+    }
+    // branch twist factors zeta_b^q = exp(2 pi i b q / K)
+    cplx zeta[K / 2];
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) zeta[q] = conjc(ldgc(&a.tw[K + ((b * q) & (K - 1))]));
+    __syncthreads();
+
     // 1. fold the (zero-padded) source block into branch b and twist
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int g = idx >> logm, r = idx & (m - 1);
-        const int rp = pair0 + g;
-        cplx v = {0.0, 0.0};
-        if (rp < npairs) {
-            const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
-            const int i1 = 2 * lp;
-            const bool has2 = i1 + 1 < a.nodes;
-            const double* x1 = a.X + (uint64_t)(pb * a.nodes + i1) * N + a.lo;
-            for (int q = 0; q < K / 2; ++q) {
-                const int j = q * m + r;
-                const cplx z = {x1[j], has2 ? x1[N + j] : 0.0};
-                if (q == 0) {
-                    v = cadd(v, z);
-                } else {
-                    const cplx zeta = conjc(ldgc(&a.tw[((b * q) & (K - 1)) << shT_K]));
-                    v = cadd(v, cmul(z, zeta));
-                }
-            }
-            if (b) v = cmulc(v, ldgc(&a.tw[(b * r) << shT_n]));  // * exp(+2 pi i b r / n)
+        const PairInfo pi = s_pair[g];
+        const double* x1 = a.X + pi.row1 * N + a.lo + r;
+        double u1[K / 2], u2[K / 2];
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            u1[q] = x1[(uint64_t)q * m];
+            u2[q] = pi.has2 ? x1[N + (uint64_t)q * m] : 0.0;
         }
+        cplx v = {u1[0], u2[0]};
+#pragma unroll
+        for (int q = 1; q < K / 2; ++q) v = cadd(v, cmul(cplx{u1[q], u2[q]}, zeta[q]));
+        if (b) v = cmulc(v, ldgc(&a.tw[n + b * r]));  // * exp(+2 pi i b r / n)
+        if (pair0 + g >= npairs) v = {0.0, 0.0};
         buf[sphys(idx)] = v;
     }
     __syncthreads();
@@ -70,60 +83,148 @@ __global__ void __launch_bounds__(kMpThreads) mp_kernel(MpArgs a) {
     fft_forward(buf, total, logm, a.tw, a.logT);
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int g = idx >> logm, r = idx & (m - 1);
-        const int rp = min(pair0 + g, npairs - 1);
-        const int pb = rp / a.pairs_per_problem;
-        const cplx s = ldgc(&a.spec[((uint64_t)pb * K + b) * m + r]);
-        buf[sphys(idx)] = cmul(buf[sphys(idx)], s);
+        const cplx sp = ldgc(&a.spec[((uint64_t)s_pair[g].pb * K + b) * m + r]);
+        buf[sphys(idx)] = cmul(buf[sphys(idx)], sp);
     }
     __syncthreads();
     fft_inverse(buf, total, logm, a.tw, a.logT);
     cluster.sync();
 
-    // 3. inverse K-point DFT across the cluster's branches (DSMEM), near field, store
-    const int slice = m / K;
-    const int halfK = K / 2;
+    // 3. inverse K-point DFT across the cluster's branches (DSMEM), near field, store.
+    //    Item (g, r): read the K branch values once, untwist by w_n^(bb r), then a
+    //    K-point DFT gives every output q in [K/2, K) of this r.
+    constexpr int logK = K == 2 ? 1 : K == 4 ? 2 : K == 8 ? 3 : 4;
+    const int logslice = logm - logK;
     const uint64_t tend = a.hi < N ? a.hi : N;
-    const int work = G * slice * halfK;
+    const int work = total >> logK;  // G * slice
+    const cplx* rb[K];
+#pragma unroll
+    for (int bb = 0; bb < K; ++bb) rb[bb] = cluster.map_shared_rank(buf, bb);
     for (int idx = threadIdx.x; idx < work; idx += blockDim.x) {
-        const int rr = idx % slice;
-        const int tmp = idx / slice;
-        const int qq = tmp % halfK;
-        const int g = tmp / halfK;
-        const int r = b * slice + rr;
-        const int q = halfK + qq;
-        const int rp = pair0 + g;
-        if (rp >= npairs) continue;
-        const uint64_t t = a.mid + (uint64_t)qq * m + r;
-        if (t >= tend) continue;
-        cplx y = {0.0, 0.0};
-        for (int bb = 0; bb < K; ++bb) {
-            const cplx* rb = cluster.map_shared_rank(buf, bb);
-            const cplx w = rb[sphys(g * m + r)];
-            const int e = (bb * (q * m + r)) & (n - 1);
-            y = cadd(y, cmul(w, ldgc(&a.tw[e << shT_n])));
-        }
-        const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
-        const int i1 = 2 * lp;
-        const bool has2 = i1 + 1 < a.nodes;
-        const uint64_t row1 = (uint64_t)(pb * a.nodes + i1);
-        const int tp = (int)(t - a.mid);
-        if (tp < a.J - 1) {  // exact near field: lags t - j < J
-            const double* cp = a.col + (uint64_t)pb * N;
-            const double* x1 = a.X + row1 * N;
-            const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
-            double s1 = 0.0, s2 = 0.0;
-            for (uint64_t j = a.mid; j-- > jlo;) {
-                const double cv = cp[t - j];
-                s1 = fma(cv, x1[j], s1);
-                if (has2) s2 = fma(cv, x1[N + j], s2);
+        const int rr = idx & ((1 << logslice) - 1);
+        const int g = idx >> logslice;
+        const int r = (b << logslice) + rr;
+        if (pair0 + g >= npairs) continue;
+        cplx wv[K];
+#pragma unroll
+        for (int bb = 0; bb < K; ++bb) wv[bb] = rb[bb][sphys((g << logm) + r)];
+        if (K > 2) {
+            const cplx w1 = ldgc(&a.tw[n + r]);  // w_n^r
+            cplx wp = w1;
+#pragma unroll
+            for (int bb = 1; bb < K; ++bb) {
+                wv[bb] = cmul(wv[bb], wp);
+                if (bb + 1 < K) wp = cmul(wp, w1);
             }
-            y.x += s1;
-            y.y += s2;
+            dft_reg<K, false>(wv);  // wv[q] = sum_bb w_bb w_n^(bb r) w_K^(bb q)
+        } else {
+            const cplx t = cmul(wv[1], ldgc(&a.tw[n + r]));
+            wv[1] = csub(wv[0], t);  // q = 1: w_2^1 = -1
         }
-        a.X[row1 * N + t] = a.rsrc[row1 * N + t] - y.x;
-        if (has2) a.X[(row1 + 1) * N + t] = a.rsrc[(row1 + 1) * N + t] - y.y;
+        const PairInfo pi = s_pair[g];
+        const uint64_t row1 = pi.row1;
+#pragma unroll
+        for (int q = K / 2; q < K; ++q) {
+            const uint64_t t = a.mid + (uint64_t)(q - K / 2) * m + r;
+            if (t >= tend) continue;
+            cplx y = wv[q];
+            const int tp = (int)(t - a.mid);
+            if (tp < a.J - 1) {  // exact near field: lags t - j < J
+                const double* cp = a.col + (uint64_t)pi.pb * N;
+                const double* x1 = a.X + row1 * N;
+                const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
+                double s1 = 0.0, s2 = 0.0;
+                for (uint64_t j = a.mid; j-- > jlo;) {
+                    const double cv = cp[t - j];
+                    s1 = fma(cv, x1[j], s1);
+                    if (pi.has2) s2 = fma(cv, x1[N + j], s2);
+                }
+                y.x += s1;
+                y.y += s2;
+            }
+            a.X[row1 * N + t] = a.rsrc[row1 * N + t] - y.x;
+            if (pi.has2) a.X[(row1 + 1) * N + t] = a.rsrc[(row1 + 1) * N + t] - y.y;
+        }
     }
     cluster.sync();
+}
+
+// ---- direct history product for small blocks --------------------------------
+// For n = 2h <= 256 the product is a small dense Toeplitz matrix applied to
+// every row (h/2 FMA per unknown, fewer than the FFT's ~30-60 instructions):
+//   R[row][mid + t'] -= sum_{j < h} col[h + t' - j] U[row][lo + j].
+// Each thread owns 16 consecutive outputs of one row; a warp spans 32 rows
+// with the same outputs so the column window is warp-uniform (SMEM
+// broadcast), and the 16x16 block products are fully unrolled on registers.
+template <int H>
+__global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
+    constexpr int TT = 16;
+    constexpr int TPR = H / TT;                      // threads per row
+    constexpr int RPC = kMpThreads / TPR;            // rows per CTA
+    constexpr int LD = H + 1;                        // padded row stride (conflict-free)
+    __shared__ double s_c[2 * H + TT];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* s_u = reinterpret_cast<double*>(smem_raw);   // [RPC][LD] source U
+    double* s_r = s_u + RPC * LD;                        // [RPC][LD] target R -> result
+    const int tid = threadIdx.x;
+    const uint64_t row0 = (uint64_t)blockIdx.x * RPC;
+    const uint64_t N = a.N;
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    const int nt = (tend - a.mid) < (uint64_t)H ? (int)(tend - a.mid) : H;  // valid targets
+    const int pb0 = (int)(row0 / a.nodes);
+    const double* colp = a.col + (uint64_t)pb0 * N;
+    for (int k = tid; k < 2 * H + TT; k += blockDim.x) s_c[k] = (k >= 1 && k < 2 * H && (uint64_t)k < N) ? colp[k] : 0.0;
+    // coalesced staging: a warp reads 32 consecutive time steps of one row
+    for (int e = tid; e < RPC * H; e += blockDim.x) {
+        const int rr = e / H, j = e - rr * H;
+        const uint64_t row = row0 + rr;
+        double uu = 0.0, rv = 0.0;
+        if (row < (uint64_t)a.rows) {
+            uu = a.X[row * N + a.lo + j];
+            if (j < nt) rv = a.rsrc[row * N + a.mid + j];
+        }
+        s_u[rr * LD + j] = uu;
+        s_r[rr * LD + j] = rv;
+    }
+    __syncthreads();
+    const int p = tid / RPC;                         // output tile
+    const int rr = tid - p * RPC;
+    const uint64_t row = row0 + rr;
+    const bool in_range = row < (uint64_t)a.rows;  // rows past the end compute on zeros
+    const int pb = in_range ? (int)(row / a.nodes) : pb0;
+    const bool uniform = (pb == pb0);
+    const double* cpx = a.col + (uint64_t)pb * N;
+    const double* u = s_u + rr * LD;
+    double acc[TT];
+#pragma unroll
+    for (int t = 0; t < TT; ++t) acc[t] = 0.0;
+    const int t1 = p * TT;
+#pragma unroll 1
+    for (int jb = 0; jb < H; jb += TT) {
+        double wv[2 * TT - 1];
+        const int base = H + t1 - jb - (TT - 1);
+#pragma unroll
+        for (int i = 0; i < 2 * TT - 1; ++i) {
+            const int k = base + i;
+            wv[i] = uniform ? s_c[k] : ((k >= 1 && (uint64_t)k < N) ? cpx[k] : 0.0);
+        }
+        double uv[TT];
+#pragma unroll
+        for (int i = 0; i < TT; ++i) uv[i] = u[jb + i];
+#pragma unroll
+        for (int jj = 0; jj < TT; ++jj)
+#pragma unroll
+            for (int t = 0; t < TT; ++t) acc[t] = fma(wv[t - jj + (TT - 1)], uv[jj], acc[t]);
+    }
+    double* rres = s_r + rr * LD + t1;
+#pragma unroll
+    for (int t = 0; t < TT; ++t) rres[t] -= acc[t];
+    __syncthreads();
+    for (int e = tid; e < RPC * H; e += blockDim.x) {
+        const int r2 = e / H, j = e - r2 * H;
+        const uint64_t rw = row0 + r2;
+        if (rw < (uint64_t)a.rows && j < nt) a.X[rw * N + a.mid + j] = s_r[r2 * LD + j];
+    }
 }
 
 // Kernel spectra of one D&C level for every problem: branch b of the column
@@ -142,7 +243,7 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
     const int b = blockIdx.x, pb = blockIdx.y;
     const int K = a.K, m = a.m, n = a.n;
-    const int logm = __ffs(m) - 1, logn = __ffs(n) - 1, logK = __ffs(K) - 1;
+    const int logm = __ffs(m) - 1;
     const double* col = a.col + (uint64_t)pb * a.N;
     const uint64_t kend = (uint64_t)n < a.N ? (uint64_t)n : a.N;
     for (int r = threadIdx.x; r < m; r += blockDim.x) {
@@ -150,10 +251,10 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
         for (int q = 0; q < K; ++q) {
             const uint64_t k = (uint64_t)q * m + r;
             const double c = (k >= (uint64_t)a.J && k < kend) ? col[k] : 0.0;
-            const cplx zeta = conjc(a.tw[((b * q) & (K - 1)) << (a.logT - logK)]);
+            const cplx zeta = conjc(a.tw[K + ((b * q) & (K - 1))]);
             v = cadd(v, cplx{c * zeta.x, c * zeta.y});
         }
-        v = cmulc(v, a.tw[(b * r) << (a.logT - logn)]);
+        v = cmulc(v, a.tw[n + b * r]);
         buf[sphys(r)] = v;
     }
     __syncthreads();
@@ -169,28 +270,62 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
 
 size_t mp_smem_bytes(int G, int m) { return sizeof(cplx) * (size_t)spad_len(G * m); }
 
-cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
-    const size_t smem = mp_smem_bytes(a.G, a.m);
+template <int K>
+static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(mp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mp_smem_bytes(1, 8192));
-        cudaFuncSetAttribute(mp_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(mp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mp_smem_bytes(1, kMpTile));
+        if (K > 8) cudaFuncSetAttribute(mp_kernel<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.K, groups, 1);
+    cfg.gridDim = dim3(K, groups, 1);
     cfg.blockDim = dim3(kMpThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = mp_smem_bytes(a.G, a.m);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = a.K;
+    attr[0].val.clusterDim.x = K;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mp_kernel, a);
+    return cudaLaunchKernelEx(&cfg, mp_kernel<K>, a);
+}
+
+template <int H>
+static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
+    constexpr int RPC = kMpThreads / (H / 16);
+    const size_t smem = sizeof(double) * 2 * RPC * (H + 1);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(mp_direct_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    const int ctas = (a.rows + RPC - 1) / RPC;
+    mp_direct_kernel<H><<<ctas, kMpThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
+
+cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
+    if (mp_is_direct(a.n)) {
+        switch (a.n / 2) {
+            case 16: return launch_direct_h<16>(a, st);
+            case 32: return launch_direct_h<32>(a, st);
+            case 64: return launch_direct_h<64>(a, st);
+            case 128: return launch_direct_h<128>(a, st);
+        }
+    }
+    switch (a.K) {
+        case 2: return launch_mp_k<2>(a, groups, st);
+        case 4: return launch_mp_k<4>(a, groups, st);
+        case 8: return launch_mp_k<8>(a, groups, st);
+        case 16: return launch_mp_k<16>(a, groups, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
@@ -198,7 +333,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mp_smem_bytes(1, 8192));
+                             (int)mp_smem_bytes(1, kMpTile));
         attr_set = true;
     }
     SpecArgs a{col, N, n, m, K, J, spec, tw, logT};

@@ -68,11 +68,14 @@ def test_direct_gpu_is_reference_order(ft, oracle_mod, cid, kw):
         assert oracle_mod.relerr(U, ref) <= 1e-13
 
 
-def test_multislab_leaf(ft, oracle_mod):
-    """Problems wider than one CTA: 8 slabs of 512 nodes exchanging scan carries."""
-    w = W.config(4, time_steps=96, cells=4097)
+@pytest.mark.parametrize("cells,steps,slabs", [(4097, 96, 8), (3001, 100, 6), (2100, 64, 5)])
+def test_multislab_leaf(ft, oracle_mod, cells, steps, slabs):
+    """Problems wider than one CTA: slabs of 512 nodes, one carry exchange per
+    leaf (phase 1 / reduced recursion / response-table correction), including
+    an uneven last slab."""
+    w = W.config(4, time_steps=steps, cells=cells)
     F, u0, phi = _inputs(oracle_mod, w)
     ref = oracle_mod.direct(w, F, u0, phi)
     plan, _, U, _ = _fast(ft, w, F, u0, phi)
-    assert plan.info.slabs == 8
+    assert plan.info.slabs == slabs
     assert oracle_mod.relerr(U, ref) <= TOL
