@@ -126,6 +126,7 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
 //   are written to xch[cta][k][2].
 template <int KIND, int NPT, int L, int MODE>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
+    extern __shared__ __align__(16) double s_out[];  // [slab nodes][L + 1] solution tile
     __shared__ double s_wt[2][32][2];
     __shared__ double s_own[2];
     __shared__ double s_cx[L][2];
@@ -168,19 +169,21 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         kB[v] = (MODE == 0 && KIND == SK_TRIDIAG && valid) ? a.kcoef[(uint64_t)pb * 2 * a.nodes + a.nodes + q] : 0.0;
     }
     const int own_t = (mreal - 1) / NPT, own_v = (mreal - 1) - own_t * NPT;
-
-#pragma unroll
-    for (int k = 0; k < L; ++k) {
-        if (k >= len) break;
+    // Rolling window: tile[v][i] holds the right-hand side of step k + i; each
+    // step shifts it down by one register while pushing the new solution into
+    // the remaining in-leaf steps (no unrolling over k: the body stays small
+    // enough for the instruction cache).
+#pragma unroll 1
+    for (int k = 0; k < len; ++k) {
         const int par = k & 1;
         double x[NPT];
         if (KIND == SK_DIAG) {
 #pragma unroll
-            for (int v = 0; v < NPT; ++v) x[v] = tile[v][k] / pc.d;
+            for (int v = 0; v < NPT; ++v) x[v] = tile[v][0] / pc.d;
         } else {
             double in[NPT];
 #pragma unroll
-            for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][k] / pc.d : tile[v][k];
+            for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] / pc.d : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
             cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, nw, Fv, Bv, totF, totB);
             double cF = totF;
@@ -207,29 +210,23 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
                 }
             }
         }
-        // in-leaf history: push x into the remaining steps of the leaf (padding
-        // nodes beyond the slab stay exactly zero)
 #pragma unroll
         for (int v = 0; v < NPT; ++v) {
-            if (tid * NPT + v >= mreal) x[v] = 0.0;
-            tile[v][k] = x[v];
+            if (tid * NPT + v >= mreal) x[v] = 0.0;  // padding nodes stay exactly zero
+            s_out[(tid * NPT + v) * (L + 1) + k] = x[v];
 #pragma unroll
-            for (int k2 = k + 1; k2 < L; ++k2) tile[v][k2] = fma(-cw[k2 - k], x[v], tile[v][k2]);
+            for (int i = 0; i + 1 < L; ++i) tile[v][i] = fma(-cw[i + 1], x[v], tile[v][i + 1]);
+            tile[v][L - 1] = 0.0;
         }
     }
 
-#pragma unroll
-    for (int v = 0; v < NPT; ++v) {
-        const int q = tid * NPT + v;
-        if (q < mreal) {
-            double* dst = a.X + (uint64_t)(pb * a.nodes + slab0 + q) * N + a.t0;
-#pragma unroll
-            for (int k = 0; k < L; ++k)
-                if (k < len) dst[k] = tile[v][k];
-        }
+    __syncthreads();
+    // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
+    for (int e = tid; e < mreal * len; e += blockDim.x) {
+        const int q = e / len, k = e - q * len;
+        a.X[(uint64_t)(pb * a.nodes + slab0 + q) * N + a.t0 + k] = s_out[q * (L + 1) + k];
     }
     if (MODE == 1) {
-        __syncthreads();
         double* xo = a.xch + (uint64_t)cta * L * 2;
         for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
     }
@@ -262,7 +259,19 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 
     // load the carries of every slab of this problem and the response tables
     const double* xin = a.xch + (uint64_t)pb * P * L * 2;
-    for (int i = tid; i < P * L * 2; i += blockDim.x) s_c0[i] = __ldcg(&xin[i]);
+    for (int i0 = 0; i0 < P * L * 2; i0 += 8 * kLeafThreads) {  // 8 loads in flight per thread
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * kLeafThreads + tid;
+            v[u] = i < P * L * 2 ? __ldcg(&xin[i]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * kLeafThreads + tid;
+            if (i < P * L * 2) s_c0[i] = v[u];
+        }
+    }
     const double* hsrc = a.resp_h + (uint64_t)pb * 2 * L * 4;
     for (int i = tid; i < 2 * L * 4; i += blockDim.x) (&s_h[0][0][0])[i] = hsrc[i];
     __syncthreads();
@@ -288,36 +297,19 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
         const double lamB = act ? lp[min(a.nodes - last_s, a.lp_stride - 1)] : 0.0;
         const double lmF = lp[min(m * lane, a.lp_stride - 1)];
         const double lmB = lp[min(m * (31 - lane), a.lp_stride - 1)];
-        double ELh[L], ERh[L];
+        // rolling accumulators: accF[i], accB[i] collect the lag responses
+        // destined for step k + i
+        double accF[L], accB[L];
 #pragma unroll
-        for (int k = 0; k < L; ++k) {
-            ELh[k] = 0.0;
-            ERh[k] = 0.0;
+        for (int i = 0; i < L; ++i) {
+            accF[i] = 0.0;
+            accB[i] = 0.0;
         }
         const int nth2 = nw2 * 32;
-#pragma unroll
-        for (int k = 0; k < L; ++k) {
-            if (k >= len) break;
-            double cF = act ? s_c0[(sl * L + k) * 2] : 0.0;
-            double cB = act ? s_c0[(sl * L + k) * 2 + 1] : 0.0;
-            double aF0 = 0.0, aF1 = 0.0, aB0 = 0.0, aB1 = 0.0;
-#pragma unroll
-            for (int l = 1; l <= k; ++l) {
-                const double* h = s_h[ht][l];
-                aF0 = fma(h[0], ELh[k - l], aF0);
-                aF1 = fma(h[1], ERh[k - l], aF1);
-                if (TRI) {
-                    aB0 = fma(h[2], ELh[k - l], aB0);
-                    aB1 = fma(h[3], ERh[k - l], aB1);
-                }
-            }
-            if (act) {
-                cF += aF0 + aF1;
-                cB += aB0 + aB1;
-            } else {
-                cF = 0.0;
-                cB = 0.0;
-            }
+#pragma unroll 1
+        for (int k = 0; k < len; ++k) {
+            double cF = act ? s_c0[(sl * L + k) * 2] + accF[0] : 0.0;
+            double cB = act ? s_c0[(sl * L + k) * 2 + 1] + accB[0] : 0.0;
             // inclusive scans over slabs (uniform multiplier lam^m)
             double SF = cF, SB = cB;
 #pragma unroll
@@ -327,7 +319,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
             }
             const double exF = exm * __shfl_up_sync(0xffffffffu, SF, 1);
             const double exB = TRI ? exbm * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
-            // double-buffered partials: one named barrier separates write and read
             double (*part)[2] = s_part[k & 1];
             if (lane == 31) part[w][0] = SF;
             if (lane == 0) part[w][1] = SB;
@@ -364,12 +355,21 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
                 EL = 0.0;
                 ER = 0.0;
             }
-            ELh[k] = EL;
-            ERh[k] = ER;
             if (sl == s) {
                 s_inj[k][0] = EL;
                 s_inj[k][1] = ER;
             }
+#pragma unroll
+            for (int i = 0; i + 1 < L; ++i) {
+                const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
+                accF[i] = fma(hF.x, EL, fma(hF.y, ER, accF[i + 1]));
+                if (TRI) {
+                    const double2 hB = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][2]);
+                    accB[i] = fma(hB.x, EL, fma(hB.y, ER, accB[i + 1]));
+                }
+            }
+            accF[L - 1] = 0.0;
+            accB[L - 1] = 0.0;
             // s_tot / s_part are rewritten next step only after its first barrier,
             // which every reader of this step has passed
         }
@@ -383,25 +383,26 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
     for (int q = tid; q < mreal; q += blockDim.x) {
         double* xr = a.X + (uint64_t)(pb * a.nodes + slab0 + q) * a.N + a.t0;
-        const double* gl = GT + (uint64_t)q * L;
-        const double* gr = GT + (uint64_t)(m + q) * L;
-        double g1[L], g2[L];
+        double corr[L];
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-            g1[l] = gl[l];
-            g2[l] = TRI ? gr[l] : 0.0;
-        }
+        for (int k = 0; k < L; ++k) corr[k] = 0.0;
+#pragma unroll 1
+        for (int side = 0; side < (TRI ? 2 : 1); ++side) {
+            const double* g = GT + (uint64_t)(side * m + q) * L;
+            double gv[L], inj[L];
 #pragma unroll
-        for (int k = 0; k < L; ++k) {
-            if (k >= len) break;
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-            for (int l = 0; l <= k; ++l) {
-                acc0 = fma(g1[l], s_inj[k - l][0], acc0);
-                if (TRI) acc1 = fma(g2[l], s_inj[k - l][1], acc1);
+            for (int l = 0; l < L; ++l) {
+                gv[l] = g[l];
+                inj[l] = s_inj[l][side];
             }
-            xr[k] += acc0 + acc1;
+#pragma unroll
+            for (int k = 0; k < L; ++k)
+#pragma unroll
+                for (int l = 0; l <= k; ++l) corr[k] = fma(gv[l], inj[k - l], corr[k]);
         }
+#pragma unroll
+        for (int k = 0; k < L; ++k)
+            if (k < len) xr[k] += corr[k];
     }
 }
 
@@ -409,11 +410,19 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool multi, cudaStream_t st) {
+    const size_t osmem = sizeof(double) * (size_t)threads * NPT * (L + 1);
+    static bool oattr = false;
+    if (!oattr) {
+        const int mx = (int)(sizeof(double) * kLeafThreads * NPT * (L + 1));
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        oattr = true;
+    }
     if (!multi) {
-        leaf_kernel<KIND, NPT, L, 0><<<ctas, threads, 0, st>>>(a);
+        leaf_kernel<KIND, NPT, L, 0><<<ctas, threads, osmem, st>>>(a);
         return cudaGetLastError();
     }
-    leaf_kernel<KIND, NPT, L, 1><<<ctas, threads, 0, st>>>(a);
+    leaf_kernel<KIND, NPT, L, 1><<<ctas, threads, osmem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(double) * (size_t)a.P * L * 2;

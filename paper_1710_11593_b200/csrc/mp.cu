@@ -174,17 +174,25 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
     const int pb0 = (int)(row0 / a.nodes);
     const double* colp = a.col + (uint64_t)pb0 * N;
     for (int k = tid; k < 2 * H + TT; k += blockDim.x) s_c[k] = (k >= 1 && k < 2 * H && (uint64_t)k < N) ? colp[k] : 0.0;
-    // coalesced staging: a warp reads 32 consecutive time steps of one row
-    for (int e = tid; e < RPC * H; e += blockDim.x) {
-        const int rr = e / H, j = e - rr * H;
-        const uint64_t row = row0 + rr;
-        double uu = 0.0, rv = 0.0;
-        if (row < (uint64_t)a.rows) {
-            uu = a.X[row * N + a.lo + j];
-            if (j < nt) rv = a.rsrc[row * N + a.mid + j];
-        }
-        s_u[rr * LD + j] = uu;
-        s_r[rr * LD + j] = rv;
+    // coalesced staging: a warp reads 32 consecutive time steps of one row; all
+    // of a thread's loads are issued before any store (memory-level parallelism)
+    constexpr int PER = RPC * H / kMpThreads;  // 16
+    double uu[PER], rv[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = tid + i * kMpThreads;
+        const int r2 = e / H, j = e - r2 * H;
+        const uint64_t row = row0 + r2;
+        const bool ok = row < (uint64_t)a.rows;
+        uu[i] = ok ? a.X[row * N + a.lo + j] : 0.0;
+        rv[i] = (ok && j < nt) ? a.rsrc[row * N + a.mid + j] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = tid + i * kMpThreads;
+        const int r2 = e / H, j = e - r2 * H;
+        s_u[r2 * LD + j] = uu[i];
+        s_r[r2 * LD + j] = rv[i];
     }
     __syncthreads();
     const int p = tid / RPC;                         // output tile
