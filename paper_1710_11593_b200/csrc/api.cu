@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,7 @@ using namespace ftb;
 namespace {
 
 thread_local std::string g_err;
+int g_leaf_dbg = getenv("FT_LEAF_DBG") ? atoi(getenv("FT_LEAF_DBG")) : 0;
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -86,6 +88,7 @@ struct ft_plan {
     double* respg_d = nullptr;    // multi-slab space-time response tables
     double* resph_d = nullptr;
     std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
+    std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf
     double* dw_d = nullptr;       // direct weights [B][N]
     double* cprime_d = nullptr;   // [B][nodes]
     double* den_d = nullptr;
@@ -209,7 +212,7 @@ void local_solve_ld(const ft_plan* p, int b, const std::vector<long double>& r, 
 // Space-time responses of a slab of ms nodes to unit left / right injections
 // (shapes lam^q, lam^(ms-1-q)) at lag 0: GL, GR [ms][L]; carry responses
 // h = (hFL, hFR, hBL, hBR)[L] (lag 0 entries are zero).
-void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][m][L]*/, double* H /*[L][4]*/) {
+void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][L][m]*/, double* H /*[L][4]*/) {
     const int L = p->L, m = p->slab;
     const double* col = p->col_h.data() + (uint64_t)b * p->N;
     const long double lam = p->lamL[b];
@@ -229,8 +232,8 @@ void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][m][L]*/, do
             H[l * 4 + side] = (double)cF;
             H[l * 4 + 2 + side] = (double)cB;
         }
-        for (int q = 0; q < m; ++q)
-            for (int l = 0; l < L; ++l) G[((uint64_t)side * m + q) * L + l] = q < ms ? (double)g[l][q] : 0.0;
+        for (int l = 0; l < L; ++l)  // time-major [side][l][q] (coalesced over q on the device)
+            for (int q = 0; q < m; ++q) G[((uint64_t)side * L + l) * m + q] = q < ms ? (double)g[l][q] : 0.0;
     }
 }
 
@@ -414,6 +417,14 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
                                       "(reduce the batch or the node count per problem)");
         }
     }
+    if ((int)count > kMaxLeafProblems) {
+        delete p;
+        return set_err(FT_EINVAL, "ft_setup_batch: at most " + std::to_string(kMaxLeafProblems) +
+                                      " problems per plan");
+    }
+    p->leafcol_h.assign(count * 32, 0.0);
+    for (uint64_t b = 0; b < count; ++b)
+        for (uint64_t j = 1; j < 32 && j < N; ++j) p->leafcol_h[b * 32 + j] = p->col_h[b * N + j];
     p->lp_stride = std::max(nodes + 2, 4098);
     std::vector<double> lampow((uint64_t)count * p->lp_stride);
     p->lamL.assign(count, 0.0L);
@@ -485,6 +496,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
              std::vector<cudaEvent_t>* evs = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
+    // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve)
+    FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     uint64_t nl = 0;
     for (size_t oi = 0; oi < p->ops.size(); ++oi) {
         const Op& op = p->ops[oi];
@@ -507,6 +520,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.xch = p->xch_d;
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
+            a.dbg = g_leaf_dbg;
             FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P, p->threads, st));
         } else {
             const Level& lv = p->levels[op.level];

@@ -28,7 +28,8 @@ struct ProblemConst {
 };
 
 constexpr int kLeafThreads = 256;
-constexpr int kMaxSlabs = 160;  // slabs per problem in the multi-slab leaf
+constexpr int kMaxSlabs = 160;
+constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in constant memory)  // slabs per problem in the multi-slab leaf
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
 constexpr int kMpDirectMaxH = 128;  // blocks n <= 256 use the direct Toeplitz kernel
@@ -69,6 +70,7 @@ struct LeafArgs {
     double* xch;               // multi-slab carries of the current leaf [B*P][L][2]
     const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
     const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
+    int dbg;                   // diagnostics: bit0 skip phase 2, bit1 skip phase 3
 };
 
 struct MpArgs {
@@ -123,6 +125,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
                         int threads, cudaStream_t st);
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
+cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
 
 }  // namespace ftb

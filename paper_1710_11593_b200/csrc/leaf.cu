@@ -25,6 +25,10 @@
 
 namespace ftb {
 
+// in-leaf history weights col[1..L) per problem, read through the constant
+// cache (CTA-uniform: the compiler keeps them in uniform registers)
+__constant__ double c_leafcol[kMaxLeafProblems][32];
+
 template <int NPT>
 struct ScanConsts {
     double lam;
@@ -56,13 +60,37 @@ __device__ __forceinline__ void scan_consts(ScanConsts<NPT>& sc, const double* l
     sc.exBmask = lane < 31 ? 1.0 : 0.0;
 }
 
+// dst[q][k] (row stride L+1) = src[(row0 + q) * N + t0 + k] for q < rows, k < len;
+// consecutive threads read consecutive steps of a node row, 8 loads in flight.
+template <int L>
+__device__ __forceinline__ void stage_rows(double* dst, const double* src, uint64_t row0, uint64_t N,
+                                           uint64_t t0, int rows, int len) {
+    const int total = rows * len;
+    for (int e0 = 0; e0 < total; e0 += 8 * kLeafThreads) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kLeafThreads + threadIdx.x;
+            const int q = e / len, k = e - q * len;
+            v[u] = e < total ? src[(row0 + q) * N + t0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kLeafThreads + threadIdx.x;
+            const int q = e / len, k = e - q * len;
+            if (e < total) dst[q * (L + 1) + k] = v[u];
+        }
+    }
+}
+
 // Forward (and, for TRIDIAG, backward) lam-decay scans over the CTA's nodes
 // with zero carry in at both ends.  Fv/Bv: scans at this thread's nodes;
 // totF: F at the CTA's last (possibly padding) node; totB: B at its first.
 template <int KIND, int NPT>
 __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanConsts<NPT>& sc,
-                                         double (*s_wt)[2], int lane, int w, int nw, double (&Fv)[NPT],
+                                         double (*s_wt)[2], int lane, int w, double (&Fv)[NPT],
                                          double (&Bv)[NPT], double& totF, double& totB) {
+    constexpr int nw = kLeafThreads / 32;
     constexpr bool TRI = KIND == SK_TRIDIAG;
     double f[NPT], bl[NPT];
     double acc = 0.0;
@@ -95,9 +123,9 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
     if (lane == 31) s_wt[w][0] = SF;
     if (lane == 0) s_wt[w][1] = SB;
     __syncthreads();
-    // cross-warp carries: short sequential chains over the (<= 8) warp totals
+    // cross-warp carries: short sequential chains over the 8 warp totals
     double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
-#pragma unroll 8
+#pragma unroll
     for (int ww = 0; ww < nw; ++ww) {
         if (ww == w) CF = runF;
         runF = fma(sc.lamW, runF, s_wt[ww][0]);
@@ -134,7 +162,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     const int cta = blockIdx.x;
     const int pb = cta / a.P, s = cta - pb * a.P;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int nw = blockDim.x >> 5;
     const ProblemConst pc = a.pc[pb];
     const int slab0 = s * a.slab;
     const int mreal = min(a.slab, a.nodes - slab0);
@@ -145,18 +172,26 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     const int len = a.len;
 
     double cw[L];
+    {
+        const double* cc = c_leafcol[pb < kMaxLeafProblems ? pb : 0];
 #pragma unroll
-    for (int j = 0; j < L; ++j) cw[j] = (j > 0 && (uint64_t)j < N) ? colp[j] : 0.0;
+        for (int j = 0; j < L; ++j) cw[j] = cc[j];
+    }
+    (void)colp;
 
+    // input tile: coalesced row reads (a warp reads consecutive steps of one
+    // node) staged through shared memory, then into the register window
+    stage_rows<L>(s_out, a.src, (uint64_t)(pb * a.nodes + slab0), N, a.t0, mreal, len);
+    __syncthreads();
     double tile[NPT][L];
 #pragma unroll
     for (int v = 0; v < NPT; ++v) {
         const int q = tid * NPT + v;
         const bool valid = q < mreal;
-        const double* src = a.src + (uint64_t)(pb * a.nodes + slab0 + q) * N + a.t0;
 #pragma unroll
-        for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? src[k] : 0.0;
+        for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? s_out[q * (L + 1) + k] : 0.0;
     }
+    __syncthreads();
     ScanConsts<NPT> sc;
     scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);
     // Dirichlet correction coefficients (SINGLE mode)
@@ -169,6 +204,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         kB[v] = (MODE == 0 && KIND == SK_TRIDIAG && valid) ? a.kcoef[(uint64_t)pb * 2 * a.nodes + a.nodes + q] : 0.0;
     }
     const int own_t = (mreal - 1) / NPT, own_v = (mreal - 1) - own_t * NPT;
+    double vmask[NPT];
+#pragma unroll
+    for (int v = 0; v < NPT; ++v) vmask[v] = (tid * NPT + v < mreal) ? 1.0 : 0.0;
+    double* outp = s_out + tid * NPT * (L + 1);
     // Rolling window: tile[v][i] holds the right-hand side of step k + i; each
     // step shifts it down by one register while pushing the new solution into
     // the remaining in-leaf steps (no unrolling over k: the body stays small
@@ -185,7 +224,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
             for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] / pc.d : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
-            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, nw, Fv, Bv, totF, totB);
+            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB);
             double cF = totF;
             if (padded) {  // F at the last real node (padding nodes carry zeros)
                 if (tid == own_t) {
@@ -212,12 +251,13 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
         }
 #pragma unroll
         for (int v = 0; v < NPT; ++v) {
-            if (tid * NPT + v >= mreal) x[v] = 0.0;  // padding nodes stay exactly zero
-            s_out[(tid * NPT + v) * (L + 1) + k] = x[v];
+            x[v] *= vmask[v];  // padding nodes stay exactly zero
+            outp[v * (L + 1)] = x[v];
 #pragma unroll
             for (int i = 0; i + 1 < L; ++i) tile[v][i] = fma(-cw[i + 1], x[v], tile[v][i + 1]);
             tile[v][L - 1] = 0.0;
         }
+        ++outp;
     }
 
     __syncthreads();
@@ -277,7 +317,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     __syncthreads();
 
     // ---- phase 2: reduced recursion (warps < nw2, lane <-> slab) ----
-    if (w < nw2) {
+    if (w < nw2 && !(a.dbg & 1)) {
         const int sl = w * 32 + lane;          // slab owned by this lane
         const bool act = sl < P;
         const int ht = (sl == P - 1) ? 1 : 0;  // response table of this slab
@@ -380,19 +420,21 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     const int slab0 = s * m;
     const int mreal = min(m, a.nodes - slab0);
     const int tsel = (s == P - 1) ? 1 : 0;
+    double* s_x = s_c0 + (uint64_t)P * L * 2;  // [m][L+1] phase-1 solution tile
+    stage_rows<L>(s_x, a.X, (uint64_t)(pb * a.nodes + slab0), a.N, a.t0, mreal, len);
+    __syncthreads();
+    // tables are time-major [side][l][q]: lanes (consecutive q) read coalesced
     const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
     for (int q = tid; q < mreal; q += blockDim.x) {
-        double* xr = a.X + (uint64_t)(pb * a.nodes + slab0 + q) * a.N + a.t0;
         double corr[L];
 #pragma unroll
         for (int k = 0; k < L; ++k) corr[k] = 0.0;
 #pragma unroll 1
         for (int side = 0; side < (TRI ? 2 : 1); ++side) {
-            const double* g = GT + (uint64_t)(side * m + q) * L;
             double gv[L], inj[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                gv[l] = g[l];
+                gv[l] = GT[((uint64_t)side * L + l) * m + q];
                 inj[l] = s_inj[l][side];
             }
 #pragma unroll
@@ -400,9 +442,14 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 #pragma unroll
                 for (int l = 0; l <= k; ++l) corr[k] = fma(gv[l], inj[k - l], corr[k]);
         }
+        double* xq = s_x + q * (L + 1);
 #pragma unroll
-        for (int k = 0; k < L; ++k)
-            if (k < len) xr[k] += corr[k];
+        for (int k = 0; k < L; ++k) xq[k] += corr[k];
+    }
+    __syncthreads();
+    for (int e = tid; e < mreal * len; e += blockDim.x) {
+        const int q = e / len, k = e - q * len;
+        a.X[(uint64_t)(pb * a.nodes + slab0 + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k];
     }
 }
 
@@ -410,7 +457,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool multi, cudaStream_t st) {
-    const size_t osmem = sizeof(double) * (size_t)threads * NPT * (L + 1);
+    const size_t osmem = sizeof(double) * (size_t)kLeafThreads * NPT * (L + 1);
     static bool oattr = false;
     if (!oattr) {
         const int mx = (int)(sizeof(double) * kLeafThreads * NPT * (L + 1));
@@ -419,21 +466,26 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
         oattr = true;
     }
     if (!multi) {
-        leaf_kernel<KIND, NPT, L, 0><<<ctas, threads, osmem, st>>>(a);
+        leaf_kernel<KIND, NPT, L, 0><<<ctas, KIND == SK_DIAG ? threads : kLeafThreads, osmem, st>>>(a);
         return cudaGetLastError();
     }
-    leaf_kernel<KIND, NPT, L, 1><<<ctas, threads, osmem, st>>>(a);
+    leaf_kernel<KIND, NPT, L, 1><<<ctas, kLeafThreads, osmem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(double) * (size_t)a.P * L * 2;
+    const size_t smem = sizeof(double) * ((size_t)a.P * L * 2 + (size_t)a.slab * (L + 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(leaf_correct<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxSlabs * L * 2 * (int)sizeof(double));
+                             (int)(sizeof(double) * (kMaxSlabs * L * 2 + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
-    leaf_correct<KIND, NPT, L><<<ctas, threads, smem, st>>>(a);
+    leaf_correct<KIND, NPT, L><<<ctas, kLeafThreads, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st) {
+    return cudaMemcpyToSymbolAsync(c_leafcol, cols_host, sizeof(double) * 32 * problems, 0,
+                                   cudaMemcpyHostToDevice, st);
 }
 
 // Supported (kind, NPT, L): register tile of NPT*L doubles per thread.
