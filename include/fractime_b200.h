@@ -132,7 +132,8 @@ int ft_assemble_rhs_grid(const ft_plan* plan, const double* forcing_grid, const 
                          const double* phi, double* rhs);
 /* Device generation of a separable forcing
  *   f_b(x, t) = sum_j a[b*nmodes+j] * trig_j(k_j pi x) * t^{p[b*nmodes+j]}
- * (trig 0 = sin, 1 = cos, 2 = 1), u0_b(x) = u0_amp[b] sin(pi x), phi likewise. */
+ * (trig 0 = sin, 1 = cos, 2 = 1, 3 = x(1-x), 4 = 1-2x), u0_b(x) = u0_amp[b] sin(pi x),
+ * phi likewise. */
 int ft_assemble_rhs_modes(const ft_plan* plan, int nmodes, const double* a, const double* k,
                           const double* p, const int* trig, const double* u0_amp,
                           const double* phi_amp, double* rhs_device);
@@ -154,6 +155,14 @@ typedef struct ft_op_time {
 } ft_op_time;
 int ft_profile_fast(ft_plan* plan, const double* rhs_device, double* u_device, ft_op_time* out,
                     uint64_t capacity, uint64_t* count);
+
+/* Host-only (no CUDA needed): the divide-and-conquer launch schedule for N
+ * steps and leaf length L -- kind 0 = leaf [t0, t0+len), kind 1 = history
+ * product from source [t0 - h, t0) onto target [t0, t0 + len) (level =
+ * log2(h / L)).  Used by the CPU test-suite to check the decomposition covers
+ * every (source, target) pair of the Toeplitz history exactly once. */
+int ft_schedule(uint64_t time_steps, uint64_t leaf, ft_op_time* out, uint64_t capacity,
+                uint64_t* count);
 
 int ft_set_stream(ft_plan* plan, void* cuda_stream);
 const char* ft_last_error(void);

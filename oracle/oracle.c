@@ -293,7 +293,7 @@ double or_normal(uint64_t* state) {
 }
 
 /* Separable forcing grid  F[i][n] = sum_j a_j trig_j(k_j pi x_i) * t_n^{p_j}
- * (trig 0 = sin, 1 = cos, 2 = 1) with x_i = i*h (i = 1..cells-1) and
+ * (trig 0 = sin, 1 = cos, 2 = 1, 3 = x(1-x), 4 = 1-2x) with x_i = i*h (i = 1..cells-1) and
  * t_n = (n + t_shift) * tau, n = 1..N  -- the reference's evaluation points
  * (schemes.cpp:403-407 diffusion; :301-302 wave with t_shift = -1/2). */
 void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double t_shift,
@@ -306,7 +306,11 @@ void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double t
             const double t = ((double)n + t_shift) * tau;
             double v = 0.0;
             for (int j = 0; j < nmodes; ++j) {
-                const double sp = trig[j] == 0 ? sin(k[j] * pi * x) : trig[j] == 1 ? cos(k[j] * pi * x) : 1.0;
+                const double sp = trig[j] == 0   ? sin(k[j] * pi * x)
+                                  : trig[j] == 1 ? cos(k[j] * pi * x)
+                                  : trig[j] == 3 ? x * (1.0 - x)
+                                  : trig[j] == 4 ? (1.0 - 2.0 * x)
+                                                 : 1.0;
                 v += a[j] * sp * pow(t, p[j]);
             }
             F[(i - 1) * N + (n - 1)] = v;

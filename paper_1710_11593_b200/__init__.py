@@ -90,7 +90,7 @@ _lib = None
 
 ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
-               "ft_profile_fast", "ft_set_stream", "ft_last_error", "ft_destroy")
+               "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy")
 
 
 def lib() -> C.CDLL:
@@ -112,6 +112,7 @@ def lib() -> C.CDLL:
         L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_set_stream.argtypes = [P, P]
         L.ft_profile_fast.argtypes = [P, P, P, C.POINTER(_OpTime), U64, C.POINTER(U64)]
+        L.ft_schedule.argtypes = [U64, U64, C.POINTER(_OpTime), U64, C.POINTER(U64)]
         L.ft_last_error.restype = C.c_char_p
         L.ft_destroy.argtypes = [P]
         L.ft_destroy.restype = None
@@ -297,6 +298,16 @@ class Plan:
         return self._solve(lib().ft_solve_direct, rhs, out)
 
 
+def schedule(time_steps: int, leaf: int = 32):
+    """The divide-and-conquer launch schedule (host-only, no GPU needed)."""
+    cap = 2 * (time_steps // leaf + 2)
+    arr = (_OpTime * cap)()
+    cnt = C.c_uint64(0)
+    _check(lib().ft_schedule(time_steps, leaf, arr, cap, C.byref(cnt)))
+    return [dict(kind=arr[i].kind, level=arr[i].level, t0=arr[i].t0, len=arr[i].len)
+            for i in range(cnt.value)]
+
+
 def solve(spec: ProblemSpec, method: SolveMethod = SolveMethod.Fast, rhs_mode: int = 0) -> SchemeSolution:
     """Reference solve(spec, method, cfg) (schemes.cpp:481-489) on the GPU."""
     t0 = time.perf_counter()
@@ -332,4 +343,4 @@ def l2_error(grid: SolutionGrid, spec: ProblemSpec) -> float:
 
 __all__ = ["FractimeError", "InvalidArgument", "DomainError", "SchemeId", "SolveMethod", "ProblemSpec",
            "SolutionGrid", "SolveReport", "SchemeSolution", "Plan", "solve", "l2_error", "lib",
-           "ABI_SYMBOLS", "FT_RHS_REFERENCE", "FT_RHS_CORRECTED_N1"]
+           "ABI_SYMBOLS", "FT_RHS_REFERENCE", "FT_RHS_CORRECTED_N1", "schedule"]

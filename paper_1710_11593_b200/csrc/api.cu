@@ -776,6 +776,35 @@ int ft_solve_direct(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
     return solve_common(p, rhs, u, rep, false);
 }
 
+int ft_schedule(uint64_t N, uint64_t L, ft_op_time* out, uint64_t cap, uint64_t* count) {
+    if (!count || N == 0 || L == 0 || (L & (L - 1))) return set_err(FT_EINVAL, "ft_schedule: bad argument");
+    ft_plan tmp;
+    tmp.N = N;
+    tmp.L = (int)L;
+    tmp.nodes = 1;
+    tmp.B = 1;
+    build_schedule(&tmp);
+    for (uint64_t i = 0; i < tmp.ops.size() && i < cap; ++i) {
+        const Op& op = tmp.ops[i];
+        ft_op_time& o = out[i];
+        o.ms = 0.f;
+        o.bytes = 0;
+        if (op.kind == OP_LEAF) {
+            o.kind = 0;
+            o.level = -1;
+            o.t0 = op.t0;
+            o.len = (uint64_t)op.len;
+        } else {
+            o.kind = 1;
+            o.level = op.level;
+            o.t0 = op.mid;
+            o.len = std::min<uint64_t>(op.hi, N) - op.mid;
+        }
+    }
+    *count = tmp.ops.size();
+    return FT_OK;
+}
+
 int ft_profile_fast(ft_plan* p, const double* rhs, double* u, ft_op_time* out, uint64_t cap,
                     uint64_t* count) {
     if (!p || !rhs || !u || !count) return set_err(FT_EINVAL, "ft_profile_fast: null argument");

@@ -88,8 +88,10 @@ __global__ void rhs_modes_kernel(RhsModesArgs a) {
         double f = 0.0;
         for (int j = 0; j < a.nmodes; ++j) {
             const int tg = a.trig[j];
-            const double sp = tg == 0 ? sin(a.k[j] * 3.14159265358979323846 * x)
+            const double sp = tg == 0   ? sin(a.k[j] * 3.14159265358979323846 * x)
                               : tg == 1 ? cos(a.k[j] * 3.14159265358979323846 * x)
+                              : tg == 3 ? x * (1.0 - x)
+                              : tg == 4 ? (1.0 - 2.0 * x)
                                         : 1.0;
             f += a.a[pb * a.nmodes + j] * sp * pow(t, a.p[pb * a.nmodes + j]);
         }

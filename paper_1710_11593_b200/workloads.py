@@ -72,6 +72,48 @@ class Workload:
         return self.B * self.nodes * self.N
 
 
+def example(eid: int, gamma: float, e: int) -> Workload:
+    """The reference's manufactured Examples 3 and 4 (proj/src/harness.cpp:69-86)
+    at h = tau = 2^-e, as used by its acceptance tables (acceptance.cpp:72-90)."""
+    n = 1 << e
+    if eid == 4:  # diffusion, u = t^3 sin(pi x)
+        spec = ProblemSpec(SchemeId.Diffusion, gamma, n, n, 1.0, 1.0)
+        a = np.array([[6.0 / math.gamma(4.0 - gamma), math.pi ** 2]])
+        p = np.array([[3.0 - gamma, 3.0]])
+        return Workload(f"example4-e{e}", [spec], a, np.array([1.0, 1.0]), p, np.array([0, 0]), None, None,
+                        "t^3 sin(pi x)")
+    if eid == 3:  # wave, u = t^3 x (1 - x)
+        spec = ProblemSpec(SchemeId.DiffusionWave, gamma, n, n, 1.0, 1.0)
+        a = np.array([[6.0 / math.gamma(4.0 - gamma), 1.0]])
+        p = np.array([[3.0 - gamma, 3.0]])
+        return Workload(f"example3-e{e}", [spec], a, np.array([1.0, 1.0]), p, np.array([3, 4]), None, None,
+                        "t^3 x (1-x)")
+    raise ValueError(eid)
+
+
+def exact_final(w: Workload) -> np.ndarray:
+    """Exact solution at t = T on the interior nodes (for the examples / configs)."""
+    s = w.specs[0]
+    x = np.arange(1, s.space_cells) * s.h()
+    t = s.time_length
+    if w.exact == "t^3 sin(pi x)":
+        return t ** 3 * np.sin(np.pi * x)
+    if w.exact == "t^3 x (1-x)":
+        return t ** 3 * x * (1 - x)
+    if w.exact == "(t^2+1) sin(pi x)":
+        return (t ** 2 + 1) * np.sin(np.pi * x)
+    if w.exact == "(t^3+t+1) sin(pi x)":
+        return (t ** 3 + t + 1) * np.sin(np.pi * x)
+    raise ValueError(w.exact)
+
+
+def l2_final(w: Workload, U: np.ndarray) -> float:
+    """Reference l2_error (schemes.cpp:525-542): final-time spatial L2 norm."""
+    s = w.specs[0]
+    e = U[:, -1] - exact_final(w)
+    return float(np.sqrt(np.sum(s.h() * e * e)))
+
+
 def config(cid: int, time_steps: Optional[int] = None, cells: Optional[int] = None,
            batch: Optional[int] = None) -> Workload:
     """BASELINE.json configs[cid-1].  time_steps < N gives the time-prefix

@@ -1,0 +1,136 @@
+"""CPU: pin the oracle (oracle/oracle.c) to the reference.
+
+* bitwise against golden outputs the unmodified reference produced
+  (tests/golden/make_golden.py, reference solve()/lower_toeplitz_forward_solve);
+* against the reference's own known-answer tests (test_weights.cpp:10-59,
+  acceptance.cpp criterion 1 and the frozen paper tables :72-90);
+* bitwise against the live reference library when oracle/_ref is built.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1710_11593_b200 import workloads as W
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD / "golden.npz")
+
+
+def test_weight_kats(oracle_mod, gold):
+    o = oracle_mod.olib()
+    w = np.empty(4)
+    o.or_weights(0.5, 4, w.ctypes.data)  # G(0.5): test_weights.cpp:10-18
+    exp = [1.0, math.sqrt(2) - 1, math.sqrt(3) - math.sqrt(2), 2 - math.sqrt(3)]
+    assert np.allclose(w, exp, rtol=1e-15, atol=0)
+    assert np.array_equal(w, gold["weights_0_0.5_4"])
+    m = np.empty(3)
+    o.or_weights(0.5, 3, m.ctypes.data)  # M(1.5) uses p = 2 - 1.5: test_weights.cpp:20-26
+    assert np.array_equal(m, gold["weights_1_1.5_3"])
+    # tail form vs series (test_weights.cpp:50-59)
+    p, k = 0.5, 1_000_000_000
+    ref = p * k ** (p - 1) * (1 + (p - 1) / (2 * k) + (p - 1) * (p - 2) / (6 * k * k))
+    assert abs(o.or_power_step(k, p) - ref) <= 1e-14 * ref
+    assert o.or_power_step(k, p) == gold["power_step_1e9_0.5"][0]
+
+
+@pytest.mark.parametrize("kind,gamma", [(0, 0.3), (1, 1.7)])
+def test_weights_telescope(oracle_mod, gold, kind, gamma):
+    """acceptance.cpp criterion 1: positive, decreasing, sum_{k<K} w_k = K^p."""
+    o = oracle_mod.olib()
+    p = (1.0 - gamma) if kind == 0 else (2.0 - gamma)  # as g_weights / m_weights form it
+    w = np.empty(2000)
+    o.or_weights(p, 2000, w.ctypes.data)
+    assert (w > 0).all() and (np.diff(w) < 0).all()
+    assert abs(w.sum() - 2000 ** p) <= 1e-12 * 2000 ** p
+    key = f"weights_{kind}_{gamma}_2000"
+    assert np.array_equal(w, gold[key])
+
+
+CASES = ["cfg1_n256", "cfg2_m16_n128", "cfg2_m31_n100", "cfg3_m16_n128", "cfg4_m32_n64", "cfg4_m4096_n16"]
+CFG = {"cfg1_n256": (1, dict(time_steps=256)), "cfg2_m16_n128": (2, dict(time_steps=128, cells=17)),
+       "cfg2_m31_n100": (2, dict(time_steps=100, cells=32)), "cfg3_m16_n128": (3, dict(time_steps=128, cells=17)),
+       "cfg4_m32_n64": (4, dict(time_steps=64, cells=33)), "cfg4_m4096_n16": (4, dict(time_steps=16, cells=4097))}
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_bitwise_vs_reference_golden(oracle_mod, gold, name):
+    """The restated direct march is bit-identical to the reference's solve(Direct)."""
+    cid, kw = CFG[name]
+    w = W.config(cid, **kw)
+    F = oracle_mod.forcing_grid(w)
+    assert np.array_equal(F, gold[f"{name}_F"]), "forcing generator drifted"
+    u0 = gold[f"{name}_u0"] if f"{name}_u0" in gold else None
+    phi = gold[f"{name}_phi"] if f"{name}_phi" in gold else None
+    U = oracle_mod.direct(w, F, u0, phi)
+    assert np.array_equal(U, gold[f"{name}_direct"])
+
+
+def test_oracle_vs_live_reference(oracle_mod):
+    L = oracle_mod.rlib()
+    if L is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(5)
+    for cid, kw in [(2, dict(time_steps=40, cells=9)), (3, dict(time_steps=33, cells=12)),
+                    (4, dict(time_steps=17, cells=65))]:
+        w = W.config(cid, **kw)
+        F = rng.standard_normal((w.nodes, w.N))
+        u0 = rng.standard_normal(w.nodes)
+        phi = rng.standard_normal(w.nodes) if cid == 3 else None
+        U = oracle_mod.direct(w, F, u0, phi)
+        Ur, _, _ = oracle_mod.ref_solve(w.specs[0], "direct", F, u0, phi)
+        assert np.array_equal(U, Ur)
+
+
+@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference")])
+def test_oracle_reproduces_paper_tables(oracle_mod, eid, key):
+    """The reference's frozen Example 3/4 L2 errors (acceptance.cpp:72-90) at
+    h = tau = 2^-3..2^-6, 5% tolerance and rates within 0.05 as the reference checks."""
+    tables = json.loads((GOLD / "tables.json").read_text())
+    for col in tables[key]:
+        errs = []
+        for e in range(3, 7):
+            w = W.example(eid, col["gamma"], e)
+            U = oracle_mod.direct(w, oracle_mod.forcing_grid(w))
+            errs.append(W.l2_final(w, U))
+        for i, err in enumerate(errs):
+            assert abs(err - col["errors"][i]) <= 0.05 * col["errors"][i]
+        for i in range(1, len(errs)):
+            assert abs(math.log2(errs[i - 1] / errs[i]) - col["rates"][i - 1]) <= 0.05
+
+
+def test_long_double_march_agrees(oracle_mod):
+    """The long-double restatement (used for corrected-mode wave parity) agrees
+    with the fp64 reference-order march to rounding on a benign case."""
+    w = W.config(2, time_steps=64, cells=17)
+    F = oracle_mod.forcing_grid(w)
+    u0 = oracle_mod.initial_grid(w, w.u0amp)
+    U = oracle_mod.direct(w, F, u0)
+    R = oracle_mod.rhs(w, F, u0)
+    Uld = oracle_mod.march_ld(w.specs[0], R)
+    assert oracle_mod.relerr(U, Uld) < 1e-13
+
+
+def test_scheme3_rhs_modes(oracle_mod):
+    """Corrected mode differs from the reference only in the n = 1 row, by c*M0*u0."""
+    w = W.config(3, time_steps=16, cells=9)
+    F = oracle_mod.forcing_grid(w)
+    u0 = oracle_mod.initial_grid(w, w.u0amp)
+    phi = oracle_mod.initial_grid(w, w.phiamp)
+    R0 = oracle_mod.rhs(w, F, u0, phi, 0)
+    R1 = oracle_mod.rhs(w, F, u0, phi, 1)
+    assert np.array_equal(R0[:, 1:], R1[:, 1:])
+    mu = np.zeros(1)
+    c = np.zeros(1)
+    oracle_mod.olib().or_constants.argtypes = [__import__("ctypes").c_int, __import__("ctypes").c_double,
+                                               __import__("ctypes").c_double, __import__("ctypes").c_void_p,
+                                               __import__("ctypes").c_void_p]
+    s = w.specs[0]
+    oracle_mod.olib().or_constants(2, s.gamma, s.tau(), mu.ctypes.data, c.ctypes.data)
+    assert np.allclose(R1[:, 0] - R0[:, 0], c[0] * u0, rtol=1e-12)
