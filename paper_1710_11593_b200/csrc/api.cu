@@ -247,9 +247,15 @@ void build_schedule(ft_plan* p) {
     for (uint64_t n = 2 * L; n <= Npad; n <<= 1) {
         Level lv;
         lv.n = (int)n;
-        lv.K = n <= 2 * (uint64_t)kMpTile ? 2 : (int)(n / kMpTile);
-        lv.m = (int)(n / lv.K);
-        lv.G = lv.m >= kMpTile ? 1 : kMpTile / lv.m;
+        if (mp_is_single((int)n)) {  // one CTA per n-point transform, G row pairs per CTA
+            lv.K = 1;
+            lv.m = (int)n;
+            lv.G = (int)n >= kMpTile ? 1 : kMpTile / (int)n;
+        } else {
+            lv.K = n <= 2 * (uint64_t)kMpTile ? 2 : (int)(n / kMpTile);
+            lv.m = (int)(n / lv.K);
+            lv.G = lv.m >= kMpTile ? 1 : kMpTile / lv.m;
+        }
         if (lv.G > pairs) lv.G = pairs;
         lv.groups = (pairs + lv.G - 1) / lv.G;
         lv.spec_off = off;
@@ -484,8 +490,12 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     for (auto& lv : p->levels) spec_total += (uint64_t)B * lv.n;
     if ((rc = alloc_copy((void**)&p->spec_d, nullptr, sizeof(cplx) * std::max<uint64_t>(spec_total, 1)))) return rc;
     for (auto& lv : p->levels) {
-        FT_CUDA(launch_spectra(p->col_d, N, (int)B, lv.n, lv.m, lv.K, p->J, p->spec_d + lv.spec_off,
-                               p->tw_d, p->logT, p->stream));
+        if (lv.K == 1)
+            FT_CUDA(launch_spectra_single(p->col_d, N, (int)B, lv.n, p->J, p->spec_d + lv.spec_off, p->tw_d,
+                                          p->stream));
+        else
+            FT_CUDA(launch_spectra(p->col_d, N, (int)B, lv.n, lv.m, lv.K, p->J, p->spec_d + lv.spec_off,
+                                   p->tw_d, p->logT, p->stream));
     }
     FT_CUDA(cudaStreamSynchronize(p->stream));
     *out = p;

@@ -205,4 +205,81 @@ __device__ __forceinline__ void fft_inverse(cplx* buf, int total, int logm, cons
     }
 }
 
+// ---- compile-time specialised transforms (the history-product hot path) ----
+// With the pass geometry known at compile time every shared-memory access of a
+// butterfly is base + immediate offset, and twiddle indices are base + j.
+__host__ __device__ constexpr int lg2c(int r) { return r == 16 ? 4 : r == 8 ? 3 : r == 4 ? 2 : 1; }
+__host__ __device__ constexpr int first_radix_c(int logm) { return (logm & 3) == 0 ? 16 : (1 << (logm & 3)); }
+
+template <int R, int LOGS, bool INV>
+__device__ __forceinline__ void pass_c(cplx* buf, int total, const cplx* __restrict__ tw) {
+    constexpr int LR = lg2c(R);
+    constexpr int LOGQ = LOGS - LR;
+    constexpr int Q = 1 << LOGQ;
+    constexpr int S = 1 << LOGS;
+    const int tasks = total >> LR;
+    for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+        const int j = t & (Q - 1);
+        const int base = ((t >> LOGQ) << LOGS) + j;
+        // physical index of base + p*Q: for Q >= 16 the padding term is linear in p
+        const int pb = sphys(base);
+        cplx v[R];
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            // phys(base + pQ) - phys(base) = pQ + (pQ >> 4) for every power-of-two Q
+            // (base % 16 < Q when Q < 16; pQ % 16 == 0 when Q >= 16)
+            const int off = p * Q + ((p * Q) >> 4);
+            v[p] = buf[pb + off];
+        }
+        if (!INV) {
+            dft_reg<R, false>(v);
+            if (Q > 1) {
+                cplx w[R];
+                pass_twiddles<R>(w, tw, S, j);
+#pragma unroll
+                for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
+            }
+        } else {
+            if (Q > 1) {
+                cplx w[R];
+                pass_twiddles<R>(w, tw, S, j);
+#pragma unroll
+                for (int q = 1; q < R; ++q) v[q] = cmulc(v[q], w[q]);
+            }
+            dft_reg<R, true>(v);
+        }
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            const int off = p * Q + ((p * Q) >> 4);
+            buf[pb + off] = v[p];
+        }
+    }
+}
+
+template <int LOGM, int LOGS, bool FIRST>
+__device__ __forceinline__ void fwd_passes_c(cplx* buf, int total, const cplx* tw) {
+    constexpr int R = FIRST ? first_radix_c(LOGM) : 16;
+    pass_c<R, LOGS, false>(buf, total, tw);
+    __syncthreads();
+    if constexpr (LOGS - lg2c(R) > 0) fwd_passes_c<LOGM, LOGS - lg2c(R), false>(buf, total, tw);
+}
+
+// inverse: same passes in reverse order (smallest group first)
+template <int LOGM, int LOGS, bool FIRST>
+__device__ __forceinline__ void inv_passes_c(cplx* buf, int total, const cplx* tw) {
+    constexpr int R = FIRST ? first_radix_c(LOGM) : 16;
+    if constexpr (LOGS - lg2c(R) > 0) inv_passes_c<LOGM, LOGS - lg2c(R), false>(buf, total, tw);
+    pass_c<R, LOGS, true>(buf, total, tw);
+    __syncthreads();
+}
+
+template <int LOGM>
+__device__ __forceinline__ void fft_forward_c(cplx* buf, int total, const cplx* tw) {
+    fwd_passes_c<LOGM, LOGM, true>(buf, total, tw);
+}
+template <int LOGM>
+__device__ __forceinline__ void fft_inverse_c(cplx* buf, int total, const cplx* tw) {
+    inv_passes_c<LOGM, LOGM, true>(buf, total, tw);
+}
+
 }  // namespace ftb

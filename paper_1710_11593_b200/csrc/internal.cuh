@@ -33,6 +33,7 @@ constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in 
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
 constexpr int kMpDirectMaxH = 128;  // blocks n <= 256 use the direct Toeplitz kernel
+constexpr int kMpSingleMaxN = 8192; // 512 <= n <= 8192: single-CTA n-point FFT kernel
 
 struct __align__(16) cplx {
     double x, y;
@@ -119,6 +120,9 @@ struct RhsModesArgs {
 struct SpecArgs;
 size_t mp_smem_bytes(int G, int m);
 bool mp_is_direct(int n);
+bool mp_is_single(int n);
+cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, int J, cplx* spec,
+                                  const cplx* tw, cudaStream_t st);
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st);
 cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
                            cplx* spec, const cplx* tw, int logT, cudaStream_t st);

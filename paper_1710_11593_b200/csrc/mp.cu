@@ -33,15 +33,15 @@ struct PairInfo {
     int has2;       // second row exists
 };
 
-template <int K>
+template <int K, int LOGM>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
     __shared__ PairInfo s_pair[kMpTile / 32];
     cg::cluster_group cluster = cg::this_cluster();
     const int b = (int)cluster.block_rank();
-    const int m = a.m, G = a.G, n = a.n;
-    const int logm = __ffs(m) - 1;
+    constexpr int m = 1 << LOGM, logm = LOGM;
+    const int G = a.G, n = a.n;
     const int total = G * m;
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
     const int pair0 = blockIdx.y * G;
@@ -59,35 +59,47 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     for (int q = 0; q < K / 2; ++q) zeta[q] = conjc(ldgc(&a.tw[K + ((b * q) & (K - 1))]));
     __syncthreads();
 
-    // 1. fold the (zero-padded) source block into branch b and twist
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int g = idx >> logm, r = idx & (m - 1);
-        const PairInfo pi = s_pair[g];
-        const double* x1 = a.X + pi.row1 * N + a.lo + r;
-        double u1[K / 2], u2[K / 2];
+    // 1. fold the (zero-padded) source block into branch b and twist.  Chunks of
+    //    CH items per thread issue all their global loads before any use.
+    constexpr int CH = K >= 16 ? 1 : 16 / K;  // loads in flight per thread: CH * K
+    for (int base = threadIdx.x; base < total; base += CH * kMpThreads) {
+        double u1[CH][K / 2], u2[CH][K / 2];
 #pragma unroll
-        for (int q = 0; q < K / 2; ++q) {
-            u1[q] = x1[(uint64_t)q * m];
-            u2[q] = pi.has2 ? x1[N + (uint64_t)q * m] : 0.0;
+        for (int c = 0; c < CH; ++c) {
+            const int idx = base + c * kMpThreads;
+            const int g = min(idx, total - 1) >> logm, r = idx & (m - 1);
+            const PairInfo pi = s_pair[g];
+            const double* x1 = a.X + pi.row1 * N + a.lo + r;
+#pragma unroll
+            for (int q = 0; q < K / 2; ++q) {
+                u1[c][q] = idx < total ? x1[(uint64_t)q * m] : 0.0;
+                u2[c][q] = (idx < total && pi.has2) ? x1[N + (uint64_t)q * m] : 0.0;
+            }
         }
-        cplx v = {u1[0], u2[0]};
 #pragma unroll
-        for (int q = 1; q < K / 2; ++q) v = cadd(v, cmul(cplx{u1[q], u2[q]}, zeta[q]));
-        if (b) v = cmulc(v, ldgc(&a.tw[n + b * r]));  // * exp(+2 pi i b r / n)
-        if (pair0 + g >= npairs) v = {0.0, 0.0};
-        buf[sphys(idx)] = v;
+        for (int c = 0; c < CH; ++c) {
+            const int idx = base + c * kMpThreads;
+            if (idx >= total) break;
+            const int g = idx >> logm, r = idx & (m - 1);
+            cplx v = {u1[c][0], u2[c][0]};
+#pragma unroll
+            for (int q = 1; q < K / 2; ++q) v = cadd(v, cmul(cplx{u1[c][q], u2[c][q]}, zeta[q]));
+            if (b) v = cmulc(v, ldgc(&a.tw[n + b * r]));  // * exp(+2 pi i b r / n)
+            if (pair0 + g >= npairs) v = {0.0, 0.0};
+            buf[sphys(idx)] = v;
+        }
     }
     __syncthreads();
 
     // 2. branch convolution: forward FFT, multiply by the kernel spectrum, inverse FFT
-    fft_forward(buf, total, logm, a.tw, a.logT);
+    fft_forward_c<LOGM>(buf, total, a.tw);
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int g = idx >> logm, r = idx & (m - 1);
         const cplx sp = ldgc(&a.spec[((uint64_t)s_pair[g].pb * K + b) * m + r]);
         buf[sphys(idx)] = cmul(buf[sphys(idx)], sp);
     }
     __syncthreads();
-    fft_inverse(buf, total, logm, a.tw, a.logT);
+    fft_inverse_c<LOGM>(buf, total, a.tw);
     cluster.sync();
 
     // 3. inverse K-point DFT across the cluster's branches (DSMEM), near field, store.
@@ -100,53 +112,273 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     const cplx* rb[K];
 #pragma unroll
     for (int bb = 0; bb < K; ++bb) rb[bb] = cluster.map_shared_rank(buf, bb);
-    for (int idx = threadIdx.x; idx < work; idx += blockDim.x) {
-        const int rr = idx & ((1 << logslice) - 1);
-        const int g = idx >> logslice;
-        const int r = (b << logslice) + rr;
-        if (pair0 + g >= npairs) continue;
-        cplx wv[K];
+    constexpr int CH2 = K >= 8 ? 1 : 8 / K;
+    for (int base = threadIdx.x; base < work; base += CH2 * kMpThreads) {
+        // prefetch the targets' current right-hand sides for every output of the chunk
+        double r1[CH2][K / 2], r2[CH2][K / 2];
 #pragma unroll
-        for (int bb = 0; bb < K; ++bb) wv[bb] = rb[bb][sphys((g << logm) + r)];
-        if (K > 2) {
-            const cplx w1 = ldgc(&a.tw[n + r]);  // w_n^r
-            cplx wp = w1;
+        for (int c = 0; c < CH2; ++c) {
+            const int idx = base + c * kMpThreads;
+            const int rr = idx & ((1 << logslice) - 1);
+            const int g = min(idx, work - 1) >> logslice;
+            const int r = (b << logslice) + rr;
+            const PairInfo pi = s_pair[g];
+            const bool ok = idx < work && pair0 + g < npairs;
 #pragma unroll
-            for (int bb = 1; bb < K; ++bb) {
-                wv[bb] = cmul(wv[bb], wp);
-                if (bb + 1 < K) wp = cmul(wp, w1);
+            for (int q = 0; q < K / 2; ++q) {
+                const uint64_t t = a.mid + (uint64_t)q * m + r;
+                const bool okt = ok && t < tend;
+                r1[c][q] = okt ? a.rsrc[pi.row1 * N + t] : 0.0;
+                r2[c][q] = (okt && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + t] : 0.0;
             }
-            dft_reg<K, false>(wv);  // wv[q] = sum_bb w_bb w_n^(bb r) w_K^(bb q)
-        } else {
-            const cplx t = cmul(wv[1], ldgc(&a.tw[n + r]));
-            wv[1] = csub(wv[0], t);  // q = 1: w_2^1 = -1
         }
-        const PairInfo pi = s_pair[g];
-        const uint64_t row1 = pi.row1;
 #pragma unroll
-        for (int q = K / 2; q < K; ++q) {
-            const uint64_t t = a.mid + (uint64_t)(q - K / 2) * m + r;
-            if (t >= tend) continue;
-            cplx y = wv[q];
-            const int tp = (int)(t - a.mid);
+        for (int c = 0; c < CH2; ++c) {
+            const int idx = base + c * kMpThreads;
+            if (idx >= work) break;
+            const int rr = idx & ((1 << logslice) - 1);
+            const int g = idx >> logslice;
+            const int r = (b << logslice) + rr;
+            if (pair0 + g >= npairs) continue;
+            cplx wv[K];
+#pragma unroll
+            for (int bb = 0; bb < K; ++bb) wv[bb] = rb[bb][sphys((g << logm) + r)];
+            if (K > 2) {
+                const cplx w1 = ldgc(&a.tw[n + r]);  // w_n^r
+                cplx wp = w1;
+#pragma unroll
+                for (int bb = 1; bb < K; ++bb) {
+                    wv[bb] = cmul(wv[bb], wp);
+                    if (bb + 1 < K) wp = cmul(wp, w1);
+                }
+                dft_reg<K, false>(wv);  // wv[q] = sum_bb w_bb w_n^(bb r) w_K^(bb q)
+            } else {
+                const cplx t = cmul(wv[1], ldgc(&a.tw[n + r]));
+                wv[1] = csub(wv[0], t);  // q = 1: w_2^1 = -1
+            }
+            const PairInfo pi = s_pair[g];
+            const uint64_t row1 = pi.row1;
+#pragma unroll
+            for (int q = K / 2; q < K; ++q) {
+                const uint64_t t = a.mid + (uint64_t)(q - K / 2) * m + r;
+                if (t >= tend) continue;
+                cplx y = wv[q];
+                const int tp = (int)(t - a.mid);
+                if (tp < a.J - 1) {  // exact near field: lags t - j < J
+                    const double* cp = a.col + (uint64_t)pi.pb * N;
+                    const double* x1 = a.X + row1 * N;
+                    const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
+                    double s1 = 0.0, s2 = 0.0;
+                    for (uint64_t j = a.mid; j-- > jlo;) {
+                        const double cv = cp[t - j];
+                        s1 = fma(cv, x1[j], s1);
+                        if (pi.has2) s2 = fma(cv, x1[N + j], s2);
+                    }
+                    y.x += s1;
+                    y.y += s2;
+                }
+                a.X[row1 * N + t] = r1[c][q - K / 2] - y.x;
+                if (pi.has2) a.X[(row1 + 1) * N + t] = r2[c][q - K / 2] - y.y;
+            }
+        }
+    }
+    cluster.sync();
+}
+
+// ---- single-CTA n-point FFT history product (512 <= n <= 8192) -------------
+// One CTA transforms G row pairs of n = 2^LOGN points (the zero-padded source
+// block).  Passes (radix 16 from S = n down, remainder radix last):
+//   * first forward pass reads U straight from HBM (the upper half is zero and
+//     pruned), writes SMEM;
+//   * last forward pass + spectrum multiply + first inverse pass are fused in
+//     registers (one SMEM round trip instead of three);
+//   * last inverse pass computes only the needed half (t in [mid, hi)) and
+//     writes R := R - y straight to HBM.
+// The spectrum (spec1_kernel) uses the same pass plan, so digit-reversed
+// orders agree.
+template <int LOGN>
+struct Plan1 {
+    static constexpr int n = 1 << LOGN;
+    static constexpr int h = n / 2;
+    static constexpr int RL = (LOGN & 3) == 0 ? 16 : (1 << (LOGN & 3));  // last (fused) radix
+    static constexpr int Q0 = n / 16;                                     // first pass stride
+};
+
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_fwd(cplx* buf, int total, const cplx* tw) {
+    // forward passes with S from LOGS down to (but excluding) the fused last one
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        pass_c<16, LOGS, false>(buf, total, tw);
+        __syncthreads();
+        mid_fwd<LOGS - 4, LOGN>(buf, total, tw);
+    }
+}
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        mid_inv<LOGS - 4, LOGN>(buf, total, tw);
+        pass_c<16, LOGS, true>(buf, total, tw);
+        __syncthreads();
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(kMpThreads, 1) mp1_kernel(MpArgs a) {
+    using PL = Plan1<LOGN>;
+    constexpr int n = PL::n, h = PL::h, Q0 = PL::Q0, RL = PL::RL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    __shared__ PairInfo s_pair[kMpTile / 512];
+    const int G = a.G;
+    const int total = G * n;
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const int pair0 = blockIdx.x * G;
+    const uint64_t N = a.N;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int rp = min(pair0 + g, npairs - 1);
+        const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+        const int i1 = 2 * lp;
+        s_pair[g] = {(uint64_t)(pb * a.nodes + i1), pb, (pair0 + g < npairs && i1 + 1 < a.nodes) ? 1 : 0};
+    }
+    __syncthreads();
+
+    // pass 0 (S = n, radix 16) from HBM; inputs p >= 8 are the zero padding
+    for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
+        const int g = t / Q0, j = t - g * Q0;
+        const PairInfo pi = s_pair[g];
+        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        const bool live = pair0 + g < npairs;
+        cplx v[16];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            v[p].x = live ? x1[(uint64_t)p * Q0] : 0.0;
+            v[p].y = (live && pi.has2) ? x1[N + (uint64_t)p * Q0] : 0.0;
+        }
+#pragma unroll
+        for (int p = 8; p < 16; ++p) v[p] = {0.0, 0.0};
+        dft_reg<16, false>(v);
+        cplx w[16];
+        pass_twiddles<16>(w, a.tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], w[q]);
+        const int pb = sphys(g * n + j);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) buf[pb + q * (Q0 + (Q0 >> 4))] = v[q];
+    }
+    __syncthreads();
+    mid_fwd<LOGN - 4, LOGN>(buf, total, a.tw);
+
+    // fused: last forward pass (S = RL, twiddle-free), spectrum, first inverse pass
+    for (int t = threadIdx.x; t < total / RL; t += blockDim.x) {
+        const int base = t * RL;
+        const int g = base >> LOGN;
+        const int pbx = sphys(base);
+        cplx v[RL];
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+        dft_reg<RL, false>(v);
+        const cplx* sp = a.spec + (uint64_t)s_pair[g].pb * n + (base & (n - 1));
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], ldgc(&sp[p]));
+        dft_reg<RL, true>(v);
+#pragma unroll
+        for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+    }
+    __syncthreads();
+    mid_inv<LOGN - 4, LOGN>(buf, total, a.tw);
+
+    // last inverse pass (S = n, radix 16): outputs p >= 8 are the targets [mid, mid + h)
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
+        const int g = t / Q0, j = t - g * Q0;
+        const PairInfo pi = s_pair[g];
+        const bool live = pair0 + g < npairs;
+        // prefetch the targets' right-hand sides
+        double r1[8], r2[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
+            const bool ok = live && tt < tend;
+            r1[p] = ok ? a.rsrc[pi.row1 * N + tt] : 0.0;
+            r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
+        }
+        const int pbx = sphys(g * n + j);
+        cplx v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = buf[pbx + q * (Q0 + (Q0 >> 4))];
+        cplx w[16];
+        pass_twiddles<16>(w, a.tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmulc(v[q], w[q]);
+        dft_reg<16, true>(v);
+        if (!live) continue;
+#pragma unroll
+        for (int p = 8; p < 16; ++p) {
+            const uint64_t tt = a.mid + j + (uint64_t)(p - 8) * Q0;
+            if (tt >= tend) continue;
+            cplx y = v[p];
+            const int tp = (int)(tt - a.mid);
             if (tp < a.J - 1) {  // exact near field: lags t - j < J
                 const double* cp = a.col + (uint64_t)pi.pb * N;
-                const double* x1 = a.X + row1 * N;
-                const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
+                const double* xr = a.X + pi.row1 * N;
+                const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
                 double s1 = 0.0, s2 = 0.0;
-                for (uint64_t j = a.mid; j-- > jlo;) {
-                    const double cv = cp[t - j];
-                    s1 = fma(cv, x1[j], s1);
-                    if (pi.has2) s2 = fma(cv, x1[N + j], s2);
+                for (uint64_t jj = a.mid; jj-- > jlo;) {
+                    const double cv = cp[tt - jj];
+                    s1 = fma(cv, xr[jj], s1);
+                    if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
                 }
                 y.x += s1;
                 y.y += s2;
             }
-            a.X[row1 * N + t] = a.rsrc[row1 * N + t] - y.x;
-            if (pi.has2) a.X[(row1 + 1) * N + t] = a.rsrc[(row1 + 1) * N + t] - y.y;
+            a.X[pi.row1 * N + tt] = r1[p - 8] - y.x;
+            if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 8] - y.y;
         }
     }
-    cluster.sync();
+}
+
+// Spectrum of one level for the single-CTA plan: full n-point column (lags
+// J <= k < min(n, N)), same passes, scaled 1/n, stored in plan order.
+template <int LOGN>
+__global__ void __launch_bounds__(kMpThreads, 1) spec1_kernel(const double* col, uint64_t N, int J, cplx* spec,
+                                                         const cplx* tw) {
+    using PL = Plan1<LOGN>;
+    constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    const int pb = blockIdx.x;
+    const double* c = col + (uint64_t)pb * N;
+    const uint64_t kend = (uint64_t)n < N ? (uint64_t)n : N;
+    for (int t = threadIdx.x; t < n / 16; t += blockDim.x) {
+        const int j = t;
+        cplx v[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const uint64_t k = (uint64_t)j + (uint64_t)p * Q0;
+            v[p] = {(k >= (uint64_t)J && k < kend) ? c[k] : 0.0, 0.0};
+        }
+        dft_reg<16, false>(v);
+        cplx w[16];
+        pass_twiddles<16>(w, tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], w[q]);
+        const int pbx = sphys(j);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) buf[pbx + q * (Q0 + (Q0 >> 4))] = v[q];
+    }
+    __syncthreads();
+    mid_fwd<LOGN - 4, LOGN>(buf, n, tw);
+    const double scale = 1.0 / (double)n;
+    for (int t = threadIdx.x; t < n / RL; t += blockDim.x) {
+        const int base = t * RL;
+        const int pbx = sphys(base);
+        cplx v[RL];
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+        dft_reg<RL, false>(v);
+#pragma unroll
+        for (int p = 0; p < RL; ++p) spec[(uint64_t)pb * n + base + p] = {v[p].x * scale, v[p].y * scale};
+    }
 }
 
 // ---- direct history product for small blocks --------------------------------
@@ -278,13 +510,13 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
 
 size_t mp_smem_bytes(int G, int m) { return sizeof(cplx) * (size_t)spad_len(G * m); }
 
-template <int K>
+template <int K, int LOGM>
 static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(mp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, kMpTile));
-        if (K > 8) cudaFuncSetAttribute(mp_kernel<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -299,7 +531,7 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mp_kernel<K>, a);
+    return cudaLaunchKernelEx(&cfg, mp_kernel<K, LOGM>, a);
 }
 
 template <int H>
@@ -317,8 +549,60 @@ static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
 }
 
 bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
+bool mp_is_single(int n) { return !mp_is_direct(n) && n >= 512 && n <= kMpSingleMaxN; }
+
+template <int LOGN>
+static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
+    constexpr int n = 1 << LOGN;
+    const size_t smem = mp_smem_bytes(a.G, n);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(mp1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mp_smem_bytes(1, n > kMpTile ? n : kMpTile));
+        attr_set = true;
+    }
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const int ctas = (npairs + a.G - 1) / a.G;
+    mp1_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int LOGN>
+static cudaError_t launch_spec1(const double* col, uint64_t N, int B, int J, cplx* spec, const cplx* tw,
+                                cudaStream_t st) {
+    constexpr int n = 1 << LOGN;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(spec1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mp_smem_bytes(1, n));
+        attr_set = true;
+    }
+    spec1_kernel<LOGN><<<B, kMpThreads, mp_smem_bytes(1, n), st>>>(col, N, J, spec, tw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, int J, cplx* spec, const cplx* tw,
+                                  cudaStream_t st) {
+    switch (n) {
+        case 512: return launch_spec1<9>(col, N, B, J, spec, tw, st);
+        case 1024: return launch_spec1<10>(col, N, B, J, spec, tw, st);
+        case 2048: return launch_spec1<11>(col, N, B, J, spec, tw, st);
+        case 4096: return launch_spec1<12>(col, N, B, J, spec, tw, st);
+        case 8192: return launch_spec1<13>(col, N, B, J, spec, tw, st);
+    }
+    return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
+    if (mp_is_single(a.n)) {
+        switch (a.n) {
+            case 512: return launch_mp1<9>(a, st);
+            case 1024: return launch_mp1<10>(a, st);
+            case 2048: return launch_mp1<11>(a, st);
+            case 4096: return launch_mp1<12>(a, st);
+            case 8192: return launch_mp1<13>(a, st);
+        }
+    }
     if (mp_is_direct(a.n)) {
         switch (a.n / 2) {
             case 16: return launch_direct_h<16>(a, st);
@@ -327,11 +611,20 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
             case 128: return launch_direct_h<128>(a, st);
         }
     }
-    switch (a.K) {
-        case 2: return launch_mp_k<2>(a, groups, st);
-        case 4: return launch_mp_k<4>(a, groups, st);
-        case 8: return launch_mp_k<8>(a, groups, st);
-        case 16: return launch_mp_k<16>(a, groups, st);
+    const int key = a.K * 100 + (__builtin_ctz(a.m));
+    switch (key) {
+        case 204: return launch_mp_k<2, 4>(a, groups, st);
+        case 205: return launch_mp_k<2, 5>(a, groups, st);
+        case 206: return launch_mp_k<2, 6>(a, groups, st);
+        case 207: return launch_mp_k<2, 7>(a, groups, st);
+        case 208: return launch_mp_k<2, 8>(a, groups, st);
+        case 209: return launch_mp_k<2, 9>(a, groups, st);
+        case 210: return launch_mp_k<2, 10>(a, groups, st);
+        case 211: return launch_mp_k<2, 11>(a, groups, st);
+        case 212: return launch_mp_k<2, 12>(a, groups, st);
+        case 412: return launch_mp_k<4, 12>(a, groups, st);
+        case 812: return launch_mp_k<8, 12>(a, groups, st);
+        case 1612: return launch_mp_k<16, 12>(a, groups, st);
     }
     return cudaErrorInvalidValue;
 }
