@@ -109,6 +109,10 @@ typedef struct ft_plan_info {
     uint64_t slabs;        /* spatial slabs (CTAs) per problem in the leaf solve */
     double h, tau;
     double mu, c;          /* SchemeConstants of problem 0 */
+    int rank, world;       /* slab partition of a partitioned plan (0, 1 otherwise) */
+    uint64_t node_begin;   /* first interior node (0-based) held by this plan */
+    uint64_t local_nodes;  /* nodes held by this plan (rows of its buffers per problem) */
+    uint64_t slabs_local;  /* slabs (CTAs) of this rank */
 } ft_plan_info;
 
 typedef struct ft_plan ft_plan;
@@ -122,6 +126,20 @@ int ft_setup(const ft_problem* problem, const ft_options* options, ft_plan** out
 int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options* options,
                    ft_plan** out);
 int ft_plan_get_info(const ft_plan* plan, ft_plan_info* info);
+
+/* Multi-GPU slab partition of one wide problem (BASELINE config 4): rank r of
+ * `world` holds the contiguous nodes [node_begin, node_begin + local_nodes)
+ * (ft_plan_info); its rhs / u buffers are [local_nodes][N].  History products
+ * are node-local; the leaf exchanges its slabs' carries once per leaf through
+ * the caller's collective: `exchange(user, count, stream)` must all-gather
+ * `count` doubles per rank from every rank's send buffer into the recv buffer
+ * (rank-major), ordered on `stream` -- e.g. ncclAllGather on that stream.  The
+ * send/recv device buffers are registered with ft_set_exchange. */
+typedef int (*ft_exchange_fn)(void* user, uint64_t count_per_rank, void* cuda_stream);
+int ft_setup_partitioned(const ft_problem* problem, const ft_options* options, int rank, int world,
+                         ft_plan** out);
+int ft_set_exchange(ft_plan* plan, ft_exchange_fn exchange, void* user, double* send_device,
+                    double* recv_device);
 int ft_column(const ft_plan* plan, uint64_t problem, double* col_host);
 
 int ft_assemble_rhs(const ft_plan* plan, ft_forcing_fn forcing, ft_initial_fn u0,

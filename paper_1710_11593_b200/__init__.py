@@ -80,15 +80,18 @@ class _OpTime(C.Structure):
 class _Info(C.Structure):
     _fields_ = [("problems", C.c_uint64), ("nodes", C.c_uint64), ("time_steps", C.c_uint64),
                 ("leaf", C.c_uint64), ("levels", C.c_uint64), ("slabs", C.c_uint64),
-                ("h", C.c_double), ("tau", C.c_double), ("mu", C.c_double), ("c", C.c_double)]
+                ("h", C.c_double), ("tau", C.c_double), ("mu", C.c_double), ("c", C.c_double),
+                ("rank", C.c_int), ("world", C.c_int), ("node_begin", C.c_uint64), ("local_nodes", C.c_uint64),
+                ("slabs_local", C.c_uint64)]
 
 
 FORCING_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_double, C.c_void_p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_void_p)
 INITIAL_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
 
 _lib = None
 
-ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
+ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exchange", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
                "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy")
 
@@ -103,6 +106,8 @@ def lib() -> C.CDLL:
         P, D, U64, I = C.c_void_p, C.POINTER(C.c_double), C.c_uint64, C.c_int
         L.ft_setup.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(P)]
         L.ft_setup_batch.argtypes = [C.POINTER(_Problem), U64, C.POINTER(_Options), C.POINTER(P)]
+        L.ft_setup_partitioned.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), I, I, C.POINTER(P)]
+        L.ft_set_exchange.argtypes = [P, EXCHANGE_FN, P, P, P]
         L.ft_plan_get_info.argtypes = [P, C.POINTER(_Info)]
         L.ft_column.argtypes = [P, U64, P]
         L.ft_assemble_rhs.argtypes = [P, FORCING_FN, INITIAL_FN, INITIAL_FN, P, P]
@@ -207,20 +212,26 @@ class Plan:
     """A device-resident solver plan (ft_setup / ft_setup_batch)."""
 
     def __init__(self, problems, rhs_mode: int = FT_RHS_REFERENCE, near_field: int = 0,
-                 device: int = -1):
+                 device: int = -1, partition=None):
         if isinstance(problems, ProblemSpec):
             problems = [problems]
         self.specs = list(problems)
         arr = (_Problem * len(self.specs))(*[p._c() for p in self.specs])
         opt = _Options(rhs_mode, near_field, device, 0)
         h = C.c_void_p()
-        _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))
+        if partition is None:
+            _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))
+        else:
+            rank, world = partition
+            _check(lib().ft_setup_partitioned(arr, C.byref(opt), rank, world, C.byref(h)))
         self._h = h
         info = _Info()
         _check(lib().ft_plan_get_info(self._h, C.byref(info)))
         self.info = info
         self.B = int(info.problems)
-        self.nodes = int(info.nodes)
+        self.nodes = int(info.local_nodes)        # rows per problem held by this plan
+        self.global_nodes = int(info.nodes)
+        self.node_begin = int(info.node_begin)
         self.N = int(info.time_steps)
 
     def __del__(self):

@@ -71,6 +71,13 @@ struct ft_plan {
     int kind = SK_DIAG;
     int L = 32, npt = 1, threads = 32, slab = 1, P = 1;
     bool multi = false;
+    // slab partition across ranks (ft_setup_partitioned); single-rank: whole problem
+    int part_rank = 0, part_world = 1;
+    int node_begin = 0, local_nodes = 1, P_local = 1;
+    ft_exchange_fn exchange = nullptr;
+    void* exchange_user = nullptr;
+    double* xsend_d = nullptr;  // caller-provided (partitioned) phase-1 carry buffer
+    bool own_xch = true;
     // levels
     std::vector<Level> levels;
     std::vector<Op> ops;
@@ -101,7 +108,7 @@ struct ft_plan {
 
 namespace {
 
-uint64_t rows_of(const ft_plan* p) { return (uint64_t)p->B * (uint64_t)p->nodes; }
+uint64_t rows_of(const ft_plan* p) { return (uint64_t)p->B * (uint64_t)p->local_nodes; }
 
 // ---- reference setup restated (weights.cpp / schemes.cpp) -------------------
 double power_step(uint64_t k, double p) {  // weights.cpp:8-16
@@ -243,7 +250,7 @@ void build_schedule(ft_plan* p) {
     while (Npad < N) Npad <<= 1;
     p->levels.clear();
     uint64_t off = 0;
-    const int pairs = (p->nodes + 1) / 2 * p->B;
+    const int pairs = (p->local_nodes + 1) / 2 * p->B;
     for (uint64_t n = 2 * L; n <= Npad; n <<= 1) {
         Level lv;
         lv.n = (int)n;
@@ -252,7 +259,8 @@ void build_schedule(ft_plan* p) {
             lv.m = (int)n;
             lv.G = (int)n >= kMpTile ? 1 : kMpTile / (int)n;
         } else {
-            lv.K = n <= 2 * (uint64_t)kMpTile ? 2 : (int)(n / kMpTile);
+            // cluster split into K branches of m <= kMpBranchMax points
+            lv.K = n <= 2 * (uint64_t)kMpBranchMax ? 2 : (int)(n / kMpBranchMax);
             lv.m = (int)(n / lv.K);
             lv.G = lv.m >= kMpTile ? 1 : kMpTile / lv.m;
         }
@@ -299,7 +307,8 @@ int ensure_work(ft_plan* p) {
     return FT_OK;
 }
 
-int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, ft_plan** out) {
+int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, ft_plan** out, int rank = 0,
+               int world = 1) {
     if (!probs || !out || count == 0) return set_err(FT_EINVAL, "ft_setup: null argument");
     *out = nullptr;
     for (uint64_t b = 0; b < count; ++b) {
@@ -401,6 +410,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
 
     // leaf configuration
     const int nodes = p->nodes;
+    p->local_nodes = nodes;
     if (p->kind == SK_DIAG) {
         p->npt = 1; p->L = 32; p->threads = 32; p->slab = 1; p->P = 1;
     } else if (nodes <= 256) {
@@ -415,13 +425,25 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         p->npt = 2; p->L = 32; p->threads = 256; p->slab = 512;
         p->P = (nodes + p->slab - 1) / p->slab;
         p->multi = true;
-        int dev_sms = 0;
-        FT_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
-        if ((int64_t)p->P * p->B > dev_sms) {
+        if (p->P > kMaxSlabs) {
             delete p;
-            return set_err(FT_EINVAL, "ft_setup: spatial slabs exceed co-resident CTAs "
-                                      "(reduce the batch or the node count per problem)");
+            return set_err(FT_EINVAL, "ft_setup: more than " + std::to_string(kMaxSlabs * 512) +
+                                          " interior nodes per problem are not supported");
         }
+    }
+    p->P_local = p->P;
+    if (world > 1) {
+        if (!p->multi || count != 1 || p->P % world != 0 || rank < 0 || rank >= world) {
+            delete p;
+            return set_err(FT_EINVAL, "ft_setup_partitioned: needs one problem wider than 2048 nodes whose " +
+                                          std::to_string(p->P) + " slabs divide evenly over " +
+                                          std::to_string(world) + " ranks");
+        }
+        p->part_rank = rank;
+        p->part_world = world;
+        p->P_local = p->P / world;
+        p->node_begin = rank * p->P_local * p->slab;
+        p->local_nodes = std::min(nodes, (rank + 1) * p->P_local * p->slab) - p->node_begin;
     }
     if ((int)count > kMaxLeafProblems) {
         delete p;
@@ -453,6 +475,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * B * nodes))) return rc;
     if (p->multi) {
         if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
+        p->xsend_d = p->xch_d;
         const uint64_t gsz = (uint64_t)2 * 2 * p->slab * p->L, hsz = (uint64_t)2 * p->L * 4;
         std::vector<double> G(B * gsz, 0.0), H(B * hsz, 0.0);
         const int mlast = nodes - (p->P - 1) * p->slab;
@@ -528,10 +551,25 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.lp_stride = p->lp_stride;
             a.kcoef = p->kcoef_d;
             a.xch = p->xch_d;
+            a.xsend = p->xsend_d;
+            a.P_local = p->P_local;
+            a.s_begin = p->part_rank * p->P_local;
+            a.node_begin = p->node_begin;
+            a.rows_pp = p->local_nodes;
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
             a.dbg = g_leaf_dbg;
-            FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P, p->threads, st));
+            FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P_local, p->threads, st));
+            if (p->multi) {
+                if (p->part_world > 1) {  // one carry all-gather per leaf (caller's collective)
+                    if (!p->exchange)
+                        return set_err(FT_EINVAL, "partitioned plan: no exchange hook (ft_set_exchange)");
+                    const int rc = p->exchange(p->exchange_user, (uint64_t)p->P_local * p->L * 2, (void*)st);
+                    if (rc) return set_err(FT_ESOLVER, "partitioned plan: exchange hook failed");
+                }
+                FT_CUDA(launch_leaf_correct(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
+                ++nl;
+            }
         } else {
             const Level& lv = p->levels[op.level];
             MpArgs a;
@@ -546,8 +584,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.K = lv.K;
             a.G = lv.G;
             a.rows = (int)rows_of(p);
-            a.nodes = p->nodes;
-            a.pairs_per_problem = (p->nodes + 1) / 2;
+            a.nodes = p->local_nodes;
+            a.pairs_per_problem = (p->local_nodes + 1) / 2;
             a.spec = p->spec_d + lv.spec_off;
             a.tw = p->tw_d;
             a.logT = p->logT;
@@ -577,6 +615,23 @@ int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options*
     return setup_impl(problems, count, options, out);
 }
 
+int ft_setup_partitioned(const ft_problem* problem, const ft_options* options, int rank, int world,
+                         ft_plan** out) {
+    return setup_impl(problem, 1, options, out, rank, world);
+}
+
+int ft_set_exchange(ft_plan* p, ft_exchange_fn fn, void* user, double* send_device, double* recv_device) {
+    if (!p || !fn || !send_device || !recv_device) return set_err(FT_EINVAL, "ft_set_exchange: null argument");
+    if (p->part_world <= 1) return set_err(FT_EINVAL, "ft_set_exchange: plan is not partitioned");
+    p->exchange = fn;
+    p->exchange_user = user;
+    p->xsend_d = send_device;
+    if (p->xch_d) cudaFree(p->xch_d);
+    p->xch_d = recv_device;
+    p->own_xch = false;
+    return FT_OK;
+}
+
 int ft_plan_get_info(const ft_plan* p, ft_plan_info* info) {
     if (!p || !info) return set_err(FT_EINVAL, "ft_plan_get_info: null argument");
     info->problems = p->B;
@@ -585,6 +640,11 @@ int ft_plan_get_info(const ft_plan* p, ft_plan_info* info) {
     info->leaf = p->L;
     info->levels = p->levels.size();
     info->slabs = p->P;
+    info->rank = p->part_rank;
+    info->world = p->part_world;
+    info->node_begin = p->node_begin;
+    info->local_nodes = p->local_nodes;
+    info->slabs_local = p->P_local;
     info->h = p->h;
     info->tau = p->tau;
     info->mu = p->mu[0];
@@ -689,11 +749,12 @@ int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const d
     RhsModesArgs ra;
     ra.R = rhs;
     ra.N = p->N;
-    ra.nodes = p->nodes;
+    ra.nodes = p->local_nodes;
     ra.B = B;
     ra.nmodes = nmodes;
     ra.scheme = p->scheme;
     ra.rhs_mode = p->rhs_mode;
+    ra.node_begin = p->node_begin;
     ra.h = p->h;
     ra.tau = p->tau;
     ra.a = a_d;
@@ -714,6 +775,7 @@ int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const d
 
 static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool fast) {
     if (!p || !rhs || !u) return set_err(FT_EINVAL, "ft_solve: null argument");
+    if (!fast && p->part_world > 1) return set_err(FT_EINVAL, "ft_solve_direct: not available on partitioned plans");
     const auto t_start = std::chrono::steady_clock::now();
     FT_CUDA(cudaSetDevice(p->device));
     const uint64_t elems = rows_of(p) * p->N;
@@ -859,6 +921,7 @@ int ft_profile_fast(ft_plan* p, const double* rhs, double* u, ft_op_time* out, u
 void ft_destroy(ft_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
+    if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
                     p->kcoef_d, p->respg_d, p->resph_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)

@@ -81,7 +81,7 @@ __global__ void rhs_modes_kernel(RhsModesArgs a) {
         const uint64_t n0 = idx % a.N;
         const uint64_t row = idx / a.N;
         const int pb = (int)(row / a.nodes);
-        const int i = (int)(row % a.nodes) + 1;
+        const int i = a.node_begin + (int)(row % a.nodes) + 1;
         const double x = a.scheme == 0 ? 0.0 : (double)i * a.h;
         const double n = (double)(n0 + 1);
         const double t = a.scheme == 2 ? (n - 0.5) * a.tau : n * a.tau;

@@ -105,6 +105,40 @@ __device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restri
     }
 }
 
+// R-point forward DFT (natural order in/out) of R/2 data points followed by R/2
+// zeros: the first radix-2 stage degenerates to v[i+R/2] = v[i] w_R^i.
+template <int R>
+__device__ __forceinline__ void dft_reg_halfzero(cplx (&v)[R]) {
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) {
+        if (R == 16) v[i + 8] = twc<16, false>(v[i], i);
+        else if (R == 8) v[i + 4] = twc<8, false>(v[i], i);
+        else if (R == 4) v[i + 2] = twc<4, false>(v[i], i);
+        else v[i + 1] = v[i];
+    }
+#pragma unroll
+    for (int s = R / 4; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int b = 0; b < R; b += 2 * s) {
+#pragma unroll
+            for (int i = 0; i < s; ++i) {
+                const cplx a = v[b + i], c = v[b + i + s];
+                v[b + i] = cadd(a, c);
+                const cplx d = csub(a, c);
+                if (s == 1) v[b + i + s] = d;
+                else if (s == 2) v[b + i + s] = twc<4, false>(d, i);
+                else if (s == 4) v[b + i + s] = twc<8, false>(d, i);
+                else v[b + i + s] = twc<16, false>(d, i);
+            }
+        }
+    }
+    cplx t[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) t[q] = v[bitrev<R>(q)];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = t[q];
+}
+
 // One in-place DIF pass over all sequences of `total` points, group size S.
 template <int R>
 __device__ __forceinline__ void fwd_pass(cplx* buf, int total, int S, const cplx* __restrict__ tw,

@@ -34,6 +34,7 @@ constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
 constexpr int kMpDirectMaxH = 128;  // blocks n <= 256 use the direct Toeplitz kernel
 constexpr int kMpSingleMaxN = 8192; // 512 <= n <= 8192: single-CTA n-point FFT kernel
+constexpr int kMpBranchMax = 4096;  // larger n: K-CTA clusters of (n / K)-point branches (8192 measured slower: 1 CTA/SM)
 
 struct __align__(16) cplx {
     double x, y;
@@ -68,7 +69,12 @@ struct LeafArgs {
     const double* lampow;      // [B][lp_stride]: lam^k, k = 0..lp_stride-1
     int lp_stride;
     const double* kcoef;       // [B][2][nodes] single-CTA Dirichlet coefficients kF, kB
-    double* xch;               // multi-slab carries of the current leaf [B*P][L][2]
+    double* xch;               // multi-slab carries of the current leaf, all slabs [B][P][L][2]
+    double* xsend;             // phase-1 output [B*P_local][L][2] (== xch unless partitioned)
+    int P_local;               // slabs (CTAs) per problem held by this plan / rank
+    int s_begin;               // first slab of this rank
+    int node_begin;            // first node of this rank (X row 0 of a problem)
+    int rows_pp;               // X rows per problem held by this plan
     const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
     const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
     int dbg;                   // diagnostics: bit0 skip phase 2, bit1 skip phase 3
@@ -105,6 +111,7 @@ struct RhsModesArgs {
     double* R;
     uint64_t N;
     int nodes, B, nmodes, scheme, rhs_mode;
+    int node_begin;       // global index of this plan's first node (partitioned plans)
     double h, tau;
     const double* a;      // [B][nmodes]
     const double* k;      // [nmodes]
@@ -128,6 +135,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
                            cplx* spec, const cplx* tw, int logT, cudaStream_t st);
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
                         int threads, cudaStream_t st);
+cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);

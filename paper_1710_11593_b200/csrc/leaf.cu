@@ -160,11 +160,12 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     __shared__ double s_cx[L][2];
 
     const int cta = blockIdx.x;
-    const int pb = cta / a.P, s = cta - pb * a.P;
+    const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const ProblemConst pc = a.pc[pb];
     const int slab0 = s * a.slab;
     const int mreal = min(a.slab, a.nodes - slab0);
+    const uint64_t rowb = (uint64_t)pb * a.rows_pp + (slab0 - a.node_begin);  // X row of node slab0
     const bool padded = mreal != (int)blockDim.x * NPT;
     const uint64_t N = a.N;
     const double* colp = a.col + (uint64_t)pb * N;
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
 
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
-    stage_rows<L>(s_out, a.src, (uint64_t)(pb * a.nodes + slab0), N, a.t0, mreal, len);
+    stage_rows<L>(s_out, a.src, rowb, N, a.t0, mreal, len);
     __syncthreads();
     double tile[NPT][L];
 #pragma unroll
@@ -264,10 +265,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
     for (int e = tid; e < mreal * len; e += blockDim.x) {
         const int q = e / len, k = e - q * len;
-        a.X[(uint64_t)(pb * a.nodes + slab0 + q) * N + a.t0 + k] = s_out[q * (L + 1) + k];
+        a.X[(rowb + q) * N + a.t0 + k] = s_out[q * (L + 1) + k];
     }
     if (MODE == 1) {
-        double* xo = a.xch + (uint64_t)cta * L * 2;
+        double* xo = a.xsend + (uint64_t)cta * L * 2;
         for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
     }
 }
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 
     constexpr bool TRI = KIND == SK_TRIDIAG;
     const int cta = blockIdx.x;
-    const int pb = cta / a.P, s = cta - pb * a.P;
+    const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int P = a.P;
     const int nw2 = (P + 31) >> 5;          // phase-2 warps
@@ -316,6 +317,30 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     for (int i = tid; i < 2 * L * 4; i += blockDim.x) (&s_h[0][0][0])[i] = hsrc[i];
     __syncthreads();
 
+    const int slab0 = s * m;
+    const int mreal = min(m, a.nodes - slab0);
+    const uint64_t rowb = (uint64_t)pb * a.rows_pp + (slab0 - a.node_begin);  // X row of node slab0
+    double* s_x = s_c0 + (uint64_t)P * L * 2;  // [m][L+1] phase-1 solution tile
+    // ---- warps >= nw2 stage the phase-1 tile for phase 3 while phase 2 runs ----
+    if (w >= nw2) {
+        const int nth = (kLeafThreads / 32 - nw2) * 32, me = tid - nw2 * 32;
+        const uint64_t row0 = rowb;
+        for (int e0 = 0; e0 < mreal * len; e0 += 8 * nth) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * nth + me;
+                const int q = e / len, k = e - q * len;
+                v[u] = e < mreal * len ? a.X[(row0 + q) * a.N + a.t0 + k] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * nth + me;
+                const int q = e / len, k = e - q * len;
+                if (e < mreal * len) s_x[q * (L + 1) + k] = v[u];
+            }
+        }
+    }
     // ---- phase 2: reduced recursion (warps < nw2, lane <-> slab) ----
     if (w < nw2 && !(a.dbg & 1)) {
         const int sl = w * 32 + lane;          // slab owned by this lane
@@ -417,12 +442,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     __syncthreads();
 
     // ---- phase 3: x = x0 + sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l) ----
-    const int slab0 = s * m;
-    const int mreal = min(m, a.nodes - slab0);
     const int tsel = (s == P - 1) ? 1 : 0;
-    double* s_x = s_c0 + (uint64_t)P * L * 2;  // [m][L+1] phase-1 solution tile
-    stage_rows<L>(s_x, a.X, (uint64_t)(pb * a.nodes + slab0), a.N, a.t0, mreal, len);
-    __syncthreads();
     // tables are time-major [side][l][q]: lanes (consecutive q) read coalesced
     const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
     for (int q = tid; q < mreal; q += blockDim.x) {
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     __syncthreads();
     for (int e = tid; e < mreal * len; e += blockDim.x) {
         const int q = e / len, k = e - q * len;
-        a.X[(uint64_t)(pb * a.nodes + slab0 + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k];
+        a.X[(rowb + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k];
     }
 }
 
@@ -470,8 +490,11 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
         return cudaGetLastError();
     }
     leaf_kernel<KIND, NPT, L, 1><<<ctas, kLeafThreads, osmem, st>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <int KIND, int NPT, int L>
+static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)a.P * L * 2 + (size_t)a.slab * (L + 1));
     static bool attr = false;
     if (!attr) {
@@ -481,6 +504,14 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
     }
     leaf_correct<KIND, NPT, L><<<ctas, kLeafThreads, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
+    if (npt == 2 && L == 32) {
+        if (kind == SK_TRIDIAG) return launch_correct_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
+        if (kind == SK_UPWIND) return launch_correct_t<SK_UPWIND, 2, 32>(a, ctas, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st) {

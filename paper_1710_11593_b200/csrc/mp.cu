@@ -223,7 +223,7 @@ __device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(kMpThreads, 1) mp1_kernel(MpArgs a) {
+__global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
     using PL = Plan1<LOGN>;
     constexpr int n = PL::n, h = PL::h, Q0 = PL::Q0, RL = PL::RL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -254,9 +254,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) mp1_kernel(MpArgs a) {
             v[p].x = live ? x1[(uint64_t)p * Q0] : 0.0;
             v[p].y = (live && pi.has2) ? x1[N + (uint64_t)p * Q0] : 0.0;
         }
-#pragma unroll
-        for (int p = 8; p < 16; ++p) v[p] = {0.0, 0.0};
-        dft_reg<16, false>(v);
+        dft_reg_halfzero<16>(v);  // inputs 8..15 are the zero padding
         cplx w[16];
         pass_twiddles<16>(w, a.tw, n, j);
 #pragma unroll
@@ -515,7 +513,7 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mp_smem_bytes(1, kMpTile));
+                             (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
         if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
@@ -622,6 +620,9 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
         case 210: return launch_mp_k<2, 10>(a, groups, st);
         case 211: return launch_mp_k<2, 11>(a, groups, st);
         case 212: return launch_mp_k<2, 12>(a, groups, st);
+        case 213: return launch_mp_k<2, 13>(a, groups, st);
+        case 413: return launch_mp_k<4, 13>(a, groups, st);
+        case 813: return launch_mp_k<8, 13>(a, groups, st);
         case 412: return launch_mp_k<4, 12>(a, groups, st);
         case 812: return launch_mp_k<8, 12>(a, groups, st);
         case 1612: return launch_mp_k<16, 12>(a, groups, st);
@@ -634,7 +635,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mp_smem_bytes(1, kMpTile));
+                             (int)mp_smem_bytes(1, kMpBranchMax));
         attr_set = true;
     }
     SpecArgs a{col, N, n, m, K, J, spec, tw, logT};

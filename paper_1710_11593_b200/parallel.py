@@ -1,0 +1,97 @@
+"""Multi-GPU execution of the fast solver.
+
+* Independent problems (config 5): `shard_problems` splits a batch over ranks;
+  each rank builds an ordinary batched plan -- no communication.
+* One wide problem (config 4): `ShardedPlan` holds rank r's contiguous slab
+  range (ft_setup_partitioned).  History products are node-local; the leaf
+  all-gathers its slabs' scan carries once per leaf through an exchange hook
+  registered with ft_set_exchange.  `torch_exchange` implements the hook with
+  torch.distributed (NCCL on GPUs; gloo for CPU tests) on the plan's stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, List, Sequence, Tuple
+
+import torch
+
+from . import EXCHANGE_FN, Plan, _check, lib
+
+
+def partition_range(count: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous block [begin, end) of `count` items for `rank` (balanced)."""
+    base, extra = divmod(count, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def shard_problems(specs: Sequence, rank: int, world: int) -> List:
+    b, e = partition_range(len(specs), rank, world)
+    return list(specs[b:e])
+
+
+def slab_partition(nodes: int, world: int, slab: int = 512) -> List[Tuple[int, int]]:
+    """Node ranges of a slab-aligned partition (what ft_setup_partitioned uses)."""
+    slabs = -(-nodes // slab)
+    if slabs % world:
+        raise ValueError(f"{slabs} slabs do not divide over {world} ranks")
+    per = slabs // world
+    return [(r * per * slab, min(nodes, (r + 1) * per * slab)) for r in range(world)]
+
+
+def torch_exchange(send: torch.Tensor, recv: torch.Tensor, stream=None, group=None) -> Callable[[int], None]:
+    """All-gather `send` (count doubles) from every rank into `recv` (rank-major)."""
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+
+    def run(count: int) -> None:
+        assert send.numel() == count and recv.numel() == count * dist.get_world_size(group)
+        ctx = torch.cuda.stream(stream) if (stream is not None and send.is_cuda) else _null()
+        with ctx:
+            if backend == "nccl":
+                dist.all_gather_into_tensor(recv, send, group=group)
+            else:
+                parts = list(recv.view(dist.get_world_size(group), -1).unbind(0))
+                dist.all_gather(parts, send, group=group)
+
+    return run
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class ShardedPlan(Plan):
+    """Rank `rank` of `world`'s share of one wide problem.  `exchange(count)` is
+    called once per leaf and must all-gather `count` doubles per rank from
+    `self.send` into `self.recv` on `self.stream`."""
+
+    def __init__(self, spec, rank: int, world: int, exchange_factory=None, device: int = -1, **kw):
+        super().__init__(spec, partition=(rank, world), device=device, **kw)
+        self.rank, self.world = rank, world
+        P_local, L = int(self.info.slabs_local), int(self.info.leaf)
+        dev = torch.device("cuda", torch.cuda.current_device() if device < 0 else device)
+        self.send = torch.zeros(P_local * L * 2, dtype=torch.float64, device=dev)
+        self.recv = torch.zeros(world * P_local * L * 2, dtype=torch.float64, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.set_stream(self.stream.cuda_stream)
+        factory = exchange_factory or (lambda send, recv, stream: torch_exchange(send, recv, stream))
+        self._exchange = factory(self.send, self.recv, self.stream)
+
+        def hook(_user, count, _stream):
+            try:
+                self._exchange(int(count))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported through the ABI return code
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._hook = EXCHANGE_FN(hook)  # keep alive
+        _check(lib().ft_set_exchange(self._h, self._hook, None, self.send.data_ptr(), self.recv.data_ptr()))
