@@ -33,6 +33,32 @@ struct PairInfo {
     int has2;       // second row exists
 };
 
+template <int LOGN>
+struct Plan1 {
+    static constexpr int n = 1 << LOGN;
+    static constexpr int h = n / 2;
+    static constexpr int RL = (LOGN & 3) == 0 ? 16 : (1 << (LOGN & 3));  // last (fused) radix
+    static constexpr int Q0 = n / 16;                                     // first pass stride
+};
+
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_fwd(cplx* buf, int total, const cplx* tw) {
+    // forward passes with S from LOGS down to (but excluding) the fused last one
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        pass_c<16, LOGS, false>(buf, total, tw);
+        __syncthreads();
+        mid_fwd<LOGS - 4, LOGN>(buf, total, tw);
+    }
+}
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        mid_inv<LOGS - 4, LOGN>(buf, total, tw);
+        pass_c<16, LOGS, true>(buf, total, tw);
+        __syncthreads();
+    }
+}
+
 template <int K, int LOGM>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -59,47 +85,74 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     for (int q = 0; q < K / 2; ++q) zeta[q] = conjc(ldgc(&a.tw[K + ((b * q) & (K - 1))]));
     __syncthreads();
 
-    // 1. fold the (zero-padded) source block into branch b and twist.  Chunks of
-    //    CH items per thread issue all their global loads before any use.
-    constexpr int CH = K >= 16 ? 1 : 16 / K;  // loads in flight per thread: CH * K
-    for (int base = threadIdx.x; base < total; base += CH * kMpThreads) {
-        double u1[CH][K / 2], u2[CH][K / 2];
+    // 1+2a. fold the (zero-padded) source block into branch b, twist, and run the
+    //    first forward pass (S = m, radix 16) straight from HBM: task (g, j) owns
+    //    the branch points r = j + p m/16, p < 16, i.e. K/2 chunk loads per point.
+    static_assert(LOGM >= 8, "cluster branches are at least 256 points");
+    constexpr int Q0 = m / 16;
+    // theta_b^(p Q0) = exp(2 pi i b p / (16 K)) for the 16 rows of a task
+    __shared__ cplx s_tq[16];
+    if (threadIdx.x < 16) s_tq[threadIdx.x] = conjc(ldgc(&a.tw[n + ((b * (int)threadIdx.x * Q0) & (n - 1))]));
+    __syncthreads();
+    for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
+        const int g = t / Q0, j = t - g * Q0;
+        const PairInfo pi = s_pair[g];
+        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        const bool live = pair0 + g < npairs;
+        cplx v[16];
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const int idx = base + c * kMpThreads;
-            const int g = min(idx, total - 1) >> logm, r = idx & (m - 1);
-            const PairInfo pi = s_pair[g];
-            const double* x1 = a.X + pi.row1 * N + a.lo + r;
+        for (int p = 0; p < 16; ++p) v[p] = {0.0, 0.0};
 #pragma unroll
-            for (int q = 0; q < K / 2; ++q) {
-                u1[c][q] = idx < total ? x1[(uint64_t)q * m] : 0.0;
-                u2[c][q] = (idx < total && pi.has2) ? x1[N + (uint64_t)q * m] : 0.0;
+        for (int q = 0; q < K / 2; ++q) {
+            double u1[16], u2[16];
+#pragma unroll
+            for (int p = 0; p < 16; ++p) {
+                const uint64_t o = (uint64_t)q * m + (uint64_t)p * Q0;
+                u1[p] = live ? x1[o] : 0.0;
+                u2[p] = (live && pi.has2) ? x1[N + o] : 0.0;
             }
-        }
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const int idx = base + c * kMpThreads;
-            if (idx >= total) break;
-            const int g = idx >> logm, r = idx & (m - 1);
-            cplx v = {u1[c][0], u2[c][0]};
-#pragma unroll
-            for (int q = 1; q < K / 2; ++q) v = cadd(v, cmul(cplx{u1[c][q], u2[c][q]}, zeta[q]));
-            if (b) v = cmulc(v, ldgc(&a.tw[n + b * r]));  // * exp(+2 pi i b r / n)
-            if (pair0 + g >= npairs) v = {0.0, 0.0};
-            buf[sphys(idx)] = v;
+            for (int p = 0; p < 16; ++p) v[p] = q == 0 ? cplx{u1[p], u2[p]} : cadd(v[p], cmul(cplx{u1[p], u2[p]}, zeta[q]));
         }
+        if (b) {
+            const cplx tj = conjc(ldgc(&a.tw[n + b * j]));  // theta_b^j
+#pragma unroll
+            for (int p = 0; p < 16; ++p) v[p] = cmul(v[p], cmul(tj, s_tq[p]));
+        }
+        dft_reg<16, false>(v);
+        cplx w[16];
+        pass_twiddles<16>(w, a.tw, m, j);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], w[q]);
+        const int pbx = sphys(g * m + j);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) buf[pbx + q * (Q0 + (Q0 >> 4))] = v[q];
     }
     __syncthreads();
+    mid_fwd<LOGM - 4, LOGM>(buf, total, a.tw);
 
-    // 2. branch convolution: forward FFT, multiply by the kernel spectrum, inverse FFT
-    fft_forward_c<LOGM>(buf, total, a.tw);
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int g = idx >> logm, r = idx & (m - 1);
-        const cplx sp = ldgc(&a.spec[((uint64_t)s_pair[g].pb * K + b) * m + r]);
-        buf[sphys(idx)] = cmul(buf[sphys(idx)], sp);
+    // 2b. fused: last forward pass (twiddle-free), branch spectrum, first inverse pass
+    {
+        constexpr int RL = Plan1<LOGM>::RL;
+        for (int t = threadIdx.x; t < total / RL; t += blockDim.x) {
+            const int base = t * RL;
+            const int g = base >> LOGM;
+            const int pbx = sphys(base);
+            cplx v[RL];
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+            dft_reg<RL, false>(v);
+            const cplx* sp = a.spec + ((uint64_t)s_pair[g].pb * K + b) * m + (base & (m - 1));
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], ldgc(&sp[p]));
+            dft_reg<RL, true>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+        }
     }
     __syncthreads();
-    fft_inverse_c<LOGM>(buf, total, a.tw);
+    mid_inv<LOGM - 4, LOGM>(buf, total, a.tw);
+    pass_c<16, LOGM, true>(buf, total, a.tw);  // last inverse pass (S = m) -> SMEM for the combine
     cluster.sync();
 
     // 3. inverse K-point DFT across the cluster's branches (DSMEM), near field, store.
@@ -196,32 +249,6 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
 //     writes R := R - y straight to HBM.
 // The spectrum (spec1_kernel) uses the same pass plan, so digit-reversed
 // orders agree.
-template <int LOGN>
-struct Plan1 {
-    static constexpr int n = 1 << LOGN;
-    static constexpr int h = n / 2;
-    static constexpr int RL = (LOGN & 3) == 0 ? 16 : (1 << (LOGN & 3));  // last (fused) radix
-    static constexpr int Q0 = n / 16;                                     // first pass stride
-};
-
-template <int LOGS, int LOGN>
-__device__ __forceinline__ void mid_fwd(cplx* buf, int total, const cplx* tw) {
-    // forward passes with S from LOGS down to (but excluding) the fused last one
-    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
-        pass_c<16, LOGS, false>(buf, total, tw);
-        __syncthreads();
-        mid_fwd<LOGS - 4, LOGN>(buf, total, tw);
-    }
-}
-template <int LOGS, int LOGN>
-__device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
-    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
-        mid_inv<LOGS - 4, LOGN>(buf, total, tw);
-        pass_c<16, LOGS, true>(buf, total, tw);
-        __syncthreads();
-    }
-}
-
 template <int LOGN>
 __global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
     using PL = Plan1<LOGN>;
@@ -388,7 +415,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) spec1_kernel(const double* col,
 // broadcast), and the 16x16 block products are fully unrolled on registers.
 template <int H>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
-    constexpr int TT = 16;
+    constexpr int TT = H < 16 ? H : 16;
     constexpr int TPR = H / TT;                      // threads per row
     constexpr int RPC = kMpThreads / TPR;            // rows per CTA
     constexpr int LD = H + 1;                        // padded row stride (conflict-free)
@@ -534,7 +561,7 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
 
 template <int H>
 static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
-    constexpr int RPC = kMpThreads / (H / 16);
+    constexpr int RPC = kMpThreads / (H / (H < 16 ? H : 16));
     const size_t smem = sizeof(double) * 2 * RPC * (H + 1);
     static bool attr_set = false;
     if (!attr_set) {
@@ -603,6 +630,7 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
     }
     if (mp_is_direct(a.n)) {
         switch (a.n / 2) {
+            case 8: return launch_direct_h<8>(a, st);
             case 16: return launch_direct_h<16>(a, st);
             case 32: return launch_direct_h<32>(a, st);
             case 64: return launch_direct_h<64>(a, st);
@@ -611,18 +639,6 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
     }
     const int key = a.K * 100 + (__builtin_ctz(a.m));
     switch (key) {
-        case 204: return launch_mp_k<2, 4>(a, groups, st);
-        case 205: return launch_mp_k<2, 5>(a, groups, st);
-        case 206: return launch_mp_k<2, 6>(a, groups, st);
-        case 207: return launch_mp_k<2, 7>(a, groups, st);
-        case 208: return launch_mp_k<2, 8>(a, groups, st);
-        case 209: return launch_mp_k<2, 9>(a, groups, st);
-        case 210: return launch_mp_k<2, 10>(a, groups, st);
-        case 211: return launch_mp_k<2, 11>(a, groups, st);
-        case 212: return launch_mp_k<2, 12>(a, groups, st);
-        case 213: return launch_mp_k<2, 13>(a, groups, st);
-        case 413: return launch_mp_k<4, 13>(a, groups, st);
-        case 813: return launch_mp_k<8, 13>(a, groups, st);
         case 412: return launch_mp_k<4, 12>(a, groups, st);
         case 812: return launch_mp_k<8, 12>(a, groups, st);
         case 1612: return launch_mp_k<16, 12>(a, groups, st);
