@@ -78,6 +78,9 @@ struct ft_plan {
     void* exchange_user = nullptr;
     double* xsend_d = nullptr;  // caller-provided (partitioned) phase-1 carry buffer
     bool own_xch = true;
+    unsigned* bar_d = nullptr;  // fused slab leaf grid barrier
+    long long* dbgclk_d = nullptr;
+    bool fused_leaf = true;
     // levels
     std::vector<Level> levels;
     std::vector<Op> ops;
@@ -476,6 +479,15 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     if (p->multi) {
         if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
         p->xsend_d = p->xch_d;
+        if ((rc = alloc_copy((void**)&p->bar_d, nullptr, sizeof(unsigned)))) return rc;
+        if ((rc = alloc_copy((void**)&p->dbgclk_d, nullptr, sizeof(long long) * 16))) return rc;
+        {
+            // the fused leaf needs every slab CTA co-resident (cooperative launch)
+            int dev_sms = 0, per_sm = 0;
+            FT_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
+            per_sm = 1;
+            p->fused_leaf = (int64_t)B * p->P_local <= (int64_t)dev_sms * per_sm && getenv("FT_FUSED_LEAF") != nullptr;  // measured slower (opt-in)
+        }
         const uint64_t gsz = (uint64_t)2 * 2 * p->slab * p->L, hsz = (uint64_t)2 * p->L * 4;
         std::vector<double> G(B * gsz, 0.0), H(B * hsz, 0.0);
         const int mlast = nodes - (p->P - 1) * p->slab;
@@ -532,6 +544,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve)
     FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     uint64_t nl = 0;
+    unsigned leaf_index = 0;
+    if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
     for (size_t oi = 0; oi < p->ops.size(); ++oi) {
         const Op& op = p->ops[oi];
         if (evs) FT_CUDA(cudaEventRecord((*evs)[oi], st));
@@ -559,8 +573,16 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
             a.dbg = g_leaf_dbg;
-            FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P_local, p->threads, st));
-            if (p->multi) {
+            a.dbg_clk = (g_leaf_dbg & 4) ? p->dbgclk_d : nullptr;
+            a.bar = p->bar_d;
+            a.bar_target = (unsigned)(leaf_index + 1) * (unsigned)(p->B * p->P_local);
+            ++leaf_index;
+            if (p->multi && p->part_world == 1 && p->fused_leaf) {
+                FT_CUDA(launch_leaf_fused(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
+            } else {
+                FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P_local, p->threads, st));
+            }
+            if (p->multi && !(p->part_world == 1 && p->fused_leaf)) {
                 if (p->part_world > 1) {  // one carry all-gather per leaf (caller's collective)
                     if (!p->exchange)
                         return set_err(FT_EINVAL, "partitioned plan: no exchange hook (ft_set_exchange)");
@@ -848,6 +870,13 @@ int ft_solve_direct(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
     return solve_common(p, rhs, u, rep, false);
 }
 
+// diagnostics: the clock64 stamps of the last slab leaf (FT_LEAF_DBG & 4)
+int ft_debug_leaf_clocks(const ft_plan* p, long long* out16) {
+    if (!p || !p->dbgclk_d) return set_err(FT_EINVAL, "no leaf clocks");
+    FT_CUDA(cudaMemcpy(out16, p->dbgclk_d, sizeof(long long) * 16, cudaMemcpyDeviceToHost));
+    return FT_OK;
+}
+
 int ft_schedule(uint64_t N, uint64_t L, ft_op_time* out, uint64_t cap, uint64_t* count) {
     if (!count || N == 0 || L == 0 || (L & (L - 1))) return set_err(FT_EINVAL, "ft_schedule: bad argument");
     ft_plan tmp;
@@ -923,7 +952,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev0) cudaEventDestroy(p->ev0);

@@ -78,6 +78,9 @@ struct LeafArgs {
     const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
     const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
     int dbg;                   // diagnostics: bit0 skip phase 2, bit1 skip phase 3
+    unsigned* bar;             // fused slab leaf: grid-barrier counter (zeroed per solve)
+    unsigned bar_target;       // value the counter reaches when every CTA of this leaf arrived
+    long long* dbg_clk;        // diagnostics: per-phase clock64 stamps of CTA 0 (null = off)
 };
 
 struct MpArgs {
@@ -136,6 +139,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
                         int threads, cudaStream_t st);
 cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);

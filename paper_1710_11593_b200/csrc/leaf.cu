@@ -65,6 +65,32 @@ __device__ __forceinline__ void scan_consts(ScanConsts<NPT>& sc, const double* l
 template <int L>
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, uint64_t row0, uint64_t N,
                                            uint64_t t0, int rows, int len) {
+    // 16-byte loads when rows are 16-byte aligned and whole (the common case:
+    // even N, full leaf); 8 double2 in flight per thread
+    if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
+        constexpr int HL = L / 2;
+        const int total = rows * HL;
+        for (int e0 = 0; e0 < total; e0 += 8 * kLeafThreads) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * kLeafThreads + threadIdx.x;
+                const int q = e / HL, k2 = e - q * HL;
+                v[u] = e < total ? __ldcg(reinterpret_cast<const double2*>(src + (row0 + q) * N + t0) + k2)
+                                 : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * kLeafThreads + threadIdx.x;
+                const int q = e / HL, k2 = e - q * HL;
+                if (e < total) {
+                    dst[q * (L + 1) + 2 * k2] = v[u].x;
+                    dst[q * (L + 1) + 2 * k2 + 1] = v[u].y;
+                }
+            }
+        }
+        return;
+    }
     const int total = rows * len;
     for (int e0 = 0; e0 < total; e0 += 8 * kLeafThreads) {
         double v[8];
@@ -80,6 +106,25 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, uint6
             const int q = e / len, k = e - q * len;
             if (e < total) dst[q * (L + 1) + k] = v[u];
         }
+    }
+}
+
+// X[row0 + q][t0 + k] = src[q][k] (row stride L+1), 16-byte stores when aligned
+template <int L>
+__device__ __forceinline__ void store_rows(double* X, const double* src, uint64_t row0, uint64_t N, uint64_t t0,
+                                           int rows, int len, int tid, int nth) {
+    if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
+        constexpr int HL = L / 2;
+        for (int e = tid; e < rows * HL; e += nth) {
+            const int q = e / HL, k2 = e - q * HL;
+            const double2 v = make_double2(src[q * (L + 1) + 2 * k2], src[q * (L + 1) + 2 * k2 + 1]);
+            reinterpret_cast<double2*>(X + (row0 + q) * N + t0)[k2] = v;
+        }
+        return;
+    }
+    for (int e = tid; e < rows * len; e += nth) {
+        const int q = e / len, k = e - q * len;
+        X[(row0 + q) * N + t0 + k] = src[q * (L + 1) + k];
     }
 }
 
@@ -153,8 +198,8 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
 //   per step the slab's exported carries (F at its last node, B at its first)
 //   are written to xch[cta][k][2].
 template <int KIND, int NPT, int L, int MODE>
-__global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
-    extern __shared__ __align__(16) double s_out[];  // [slab nodes][L + 1] solution tile
+__device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x) {
+    // s_out: [slab nodes][L + 1] solution tile (stays resident for the fused leaf)
     __shared__ double s_wt[2][32][2];
     __shared__ double s_own[2];
     __shared__ double s_cx[L][2];
@@ -180,6 +225,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     }
     (void)colp;
 
+    const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) a.dbg_clk[8] = clock64();
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
     stage_rows<L>(s_out, a.src, rowb, N, a.t0, mreal, len);
@@ -195,6 +242,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     __syncthreads();
     ScanConsts<NPT> sc;
     scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);
+    if (stamp) a.dbg_clk[9] = clock64();
     // Dirichlet correction coefficients (SINGLE mode)
     double kF[NPT], kB[NPT];
 #pragma unroll
@@ -212,8 +260,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     // Rolling window: tile[v][i] holds the right-hand side of step k + i; each
     // step shifts it down by one register while pushing the new solution into
     // the remaining in-leaf steps (no unrolling over k: the body stays small
-    // enough for the instruction cache).
-#pragma unroll 1
+    // enough for the instruction cache).  Unrolled by two so the off-critical
+    // push FMAs of step k can be scheduled under the scan latency of step k+1.
+#pragma unroll 2
     for (int k = 0; k < len; ++k) {
         const int par = k & 1;
         double x[NPT];
@@ -262,24 +311,28 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     }
 
     __syncthreads();
+    if (stamp) a.dbg_clk[10] = clock64();
     // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
-    for (int e = tid; e < mreal * len; e += blockDim.x) {
-        const int q = e / len, k = e - q * len;
-        a.X[(rowb + q) * N + a.t0 + k] = s_out[q * (L + 1) + k];
-    }
+    if (write_x) store_rows<L>(a.X, s_out, rowb, N, a.t0, mreal, len, tid, blockDim.x);
     if (MODE == 1) {
         double* xo = a.xsend + (uint64_t)cta * L * 2;
         for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
     }
+    if (stamp) a.dbg_clk[11] = clock64();
+}
+
+template <int KIND, int NPT, int L, int MODE>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn0[];
+    leaf_body<KIND, NPT, L, MODE>(a, s_dyn0, true);
 }
 
 // Phase 2 + 3 of the slab decomposition (see file header).  One CTA per slab;
 // phase 2 runs on the first ceil(P/32) warps (one slab per lane) and is
 // replayed redundantly by every CTA (no second exchange).
 template <int KIND, int NPT, int L>
-__global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
-    extern __shared__ __align__(16) double s_dyn[];
-    double* s_c0 = s_dyn;                   // [P][L][2] phase-1 carries of every slab
+__device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, double* s_x, bool x_resident) {
+    // s_c0: [P][L][2] phase-1 carries of every slab; s_x: [m][L+1] phase-1 solution tile
     __shared__ double s_h[2][L][4];         // lag responses (main slab, last slab): hFL hFR hBL hBR
     __shared__ double s_inj[L][2];          // this slab's EL_k, ER_k
     __shared__ double s_part[2][8][2];      // cross-warp scan partials (double buffered)
@@ -298,6 +351,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     const int m = a.slab;
     const int mlast = a.nodes - (P - 1) * m;
 
+    const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) a.dbg_clk[0] = clock64();
     // load the carries of every slab of this problem and the response tables
     const double* xin = a.xch + (uint64_t)pb * P * L * 2;
     for (int i0 = 0; i0 < P * L * 2; i0 += 8 * kLeafThreads) {  // 8 loads in flight per thread
@@ -320,24 +375,39 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     const int slab0 = s * m;
     const int mreal = min(m, a.nodes - slab0);
     const uint64_t rowb = (uint64_t)pb * a.rows_pp + (slab0 - a.node_begin);  // X row of node slab0
-    double* s_x = s_c0 + (uint64_t)P * L * 2;  // [m][L+1] phase-1 solution tile
+    if (stamp) a.dbg_clk[1] = clock64();
     // ---- warps >= nw2 stage the phase-1 tile for phase 3 while phase 2 runs ----
-    if (w >= nw2) {
+    if (w >= nw2 && !x_resident) {
         const int nth = (kLeafThreads / 32 - nw2) * 32, me = tid - nw2 * 32;
-        const uint64_t row0 = rowb;
-        for (int e0 = 0; e0 < mreal * len; e0 += 8 * nth) {
-            double v[8];
+        constexpr int HL = L / 2;
+        const bool vec = len == L && (a.N & 1) == 0 && (a.t0 & 1) == 0;
+        const int total = vec ? mreal * HL : mreal * len;
+        for (int e0 = 0; e0 < total; e0 += 8 * nth) {
+            double2 v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int e = e0 + u * nth + me;
-                const int q = e / len, k = e - q * len;
-                v[u] = e < mreal * len ? a.X[(row0 + q) * a.N + a.t0 + k] : 0.0;
+                if (vec) {
+                    const int q = e / HL, k2 = e - q * HL;
+                    v[u] = e < total ? __ldcg(reinterpret_cast<const double2*>(a.X + (rowb + q) * a.N + a.t0) + k2)
+                                     : make_double2(0.0, 0.0);
+                } else {
+                    const int q = e / len, k = e - q * len;
+                    v[u] = make_double2(e < total ? a.X[(rowb + q) * a.N + a.t0 + k] : 0.0, 0.0);
+                }
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int e = e0 + u * nth + me;
-                const int q = e / len, k = e - q * len;
-                if (e < mreal * len) s_x[q * (L + 1) + k] = v[u];
+                if (e >= total) continue;
+                if (vec) {
+                    const int q = e / HL, k2 = e - q * HL;
+                    s_x[q * (L + 1) + 2 * k2] = v[u].x;
+                    s_x[q * (L + 1) + 2 * k2 + 1] = v[u].y;
+                } else {
+                    const int q = e / len, k = e - q * len;
+                    s_x[q * (L + 1) + k] = v[u].x;
+                }
             }
         }
     }
@@ -371,7 +441,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
             accB[i] = 0.0;
         }
         const int nth2 = nw2 * 32;
-#pragma unroll 1
+#pragma unroll 2
         for (int k = 0; k < len; ++k) {
             double cF = act ? s_c0[(sl * L + k) * 2] + accF[0] : 0.0;
             double cB = act ? s_c0[(sl * L + k) * 2 + 1] + accB[0] : 0.0;
@@ -424,6 +494,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
                 s_inj[k][0] = EL;
                 s_inj[k][1] = ER;
             }
+            if (a.dbg & 8) continue;  // timing ablation only (wrong results)
 #pragma unroll
             for (int i = 0; i + 1 < L; ++i) {
                 const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
@@ -441,6 +512,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     }
     __syncthreads();
 
+    if (stamp) a.dbg_clk[2] = clock64();
     // ---- phase 3: x = x0 + sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l) ----
     const int tsel = (s == P - 1) ? 1 : 0;
     // tables are time-major [side][l][q]: lanes (consecutive q) read coalesced
@@ -467,10 +539,36 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
         for (int k = 0; k < L; ++k) xq[k] += corr[k];
     }
     __syncthreads();
-    for (int e = tid; e < mreal * len; e += blockDim.x) {
-        const int q = e / len, k = e - q * len;
-        a.X[(rowb + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k];
+    if (stamp) a.dbg_clk[3] = clock64();
+    store_rows<L>(a.X, s_x, rowb, a.N, a.t0, mreal, len, tid, blockDim.x);
+    if (stamp) a.dbg_clk[4] = clock64();
+}
+
+template <int KIND, int NPT, int L>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    correct_body<KIND, NPT, L>(a, s_dyn, s_dyn + (uint64_t)a.P * L * 2, false);
+}
+
+// Single-GPU slab leaf in ONE cooperative kernel: phase 1, publish carries, a
+// grid barrier (all slabs co-resident), phases 2 + 3 on the resident tile.
+template <int KIND, int NPT, int L>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    double* s_c0 = s_dyn;
+    double* s_x = s_dyn + (uint64_t)a.P * L * 2;
+    leaf_body<KIND, NPT, L, 1>(a, s_x, false);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(a.bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+        } while (v < a.bar_target);
     }
+    __syncthreads();
+    correct_body<KIND, NPT, L>(a, s_c0, s_x, true);
 }
 
 // ---- host launch -------------------------------------------------------------
@@ -504,6 +602,28 @@ static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st
     }
     leaf_correct<KIND, NPT, L><<<ctas, kLeafThreads, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int KIND, int NPT, int L>
+static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)a.P * L * 2 + (size_t)kLeafThreads * NPT * (L + 1));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * (kMaxSlabs * L * 2 + kLeafThreads * NPT * (L + 1))));
+        attr = true;
+    }
+    void* args[] = {(void*)&a};
+    return cudaLaunchCooperativeKernel((const void*)leaf_fused<KIND, NPT, L>, dim3(ctas), dim3(kLeafThreads),
+                                       args, smem, st);
+}
+
+cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
+    if (npt == 2 && L == 32) {
+        if (kind == SK_TRIDIAG) return launch_fused_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
+        if (kind == SK_UPWIND) return launch_fused_t<SK_UPWIND, 2, 32>(a, ctas, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
