@@ -32,8 +32,8 @@ constexpr int kMaxSlabs = 160;
 constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in constant memory)  // slabs per problem in the multi-slab leaf
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
-constexpr int kMpDirectMaxH = 128;  // blocks n <= 256 use the direct Toeplitz kernel
-constexpr int kMpSingleMaxN = 8192; // 512 <= n <= 8192: single-CTA n-point FFT kernel
+constexpr int kMpDirectMaxH = 64;   // blocks n <= 128 use the direct Toeplitz kernel
+constexpr int kMpSingleMaxN = 8192; // 256 <= n <= 8192: single-CTA n-point FFT kernel
 constexpr int kMpBranchMax = 4096;  // larger n: K-CTA clusters of (n / K)-point branches (8192 measured slower: 1 CTA/SM)
 
 struct __align__(16) cplx {

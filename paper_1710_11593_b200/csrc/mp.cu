@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
     constexpr int n = PL::n, h = PL::h, Q0 = PL::Q0, RL = PL::RL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
-    __shared__ PairInfo s_pair[kMpTile / 512];
+    __shared__ PairInfo s_pair[kMpTile / 256];
     const int G = a.G;
     const int total = G * n;
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
@@ -464,14 +464,24 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
 #pragma unroll
     for (int t = 0; t < TT; ++t) acc[t] = 0.0;
     const int t1 = p * TT;
+    // CTAs spanning two problems (batched plans whose node count is not a
+    // multiple of the rows per CTA) take their column from global memory
+    const double* cwin = uniform ? s_c : nullptr;
+    double* s_cx = s_r + RPC * LD;  // per-thread fallback window (unused when uniform)
+    (void)s_cx;
 #pragma unroll 1
     for (int jb = 0; jb < H; jb += TT) {
         double wv[2 * TT - 1];
         const int base = H + t1 - jb - (TT - 1);
+        if (cwin) {
 #pragma unroll
-        for (int i = 0; i < 2 * TT - 1; ++i) {
-            const int k = base + i;
-            wv[i] = uniform ? s_c[k] : ((k >= 1 && (uint64_t)k < N) ? cpx[k] : 0.0);
+            for (int i = 0; i < 2 * TT - 1; ++i) wv[i] = cwin[base + i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < 2 * TT - 1; ++i) {
+                const int k = base + i;
+                wv[i] = (k >= 1 && (uint64_t)k < N) ? cpx[k] : 0.0;
+            }
         }
         double uv[TT];
 #pragma unroll
@@ -574,7 +584,7 @@ static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
 }
 
 bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
-bool mp_is_single(int n) { return !mp_is_direct(n) && n >= 512 && n <= kMpSingleMaxN; }
+bool mp_is_single(int n) { return !mp_is_direct(n) && n >= 256 && n <= kMpSingleMaxN; }
 
 template <int LOGN>
 static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
@@ -609,6 +619,7 @@ static cudaError_t launch_spec1(const double* col, uint64_t N, int B, int J, cpl
 cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, int J, cplx* spec, const cplx* tw,
                                   cudaStream_t st) {
     switch (n) {
+        case 256: return launch_spec1<8>(col, N, B, J, spec, tw, st);
         case 512: return launch_spec1<9>(col, N, B, J, spec, tw, st);
         case 1024: return launch_spec1<10>(col, N, B, J, spec, tw, st);
         case 2048: return launch_spec1<11>(col, N, B, J, spec, tw, st);
@@ -621,6 +632,7 @@ cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, i
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
     if (mp_is_single(a.n)) {
         switch (a.n) {
+            case 256: return launch_mp1<8>(a, st);
             case 512: return launch_mp1<9>(a, st);
             case 1024: return launch_mp1<10>(a, st);
             case 2048: return launch_mp1<11>(a, st);
