@@ -79,6 +79,8 @@ struct ft_plan {
     double* xsend_d = nullptr;  // caller-provided (partitioned) phase-1 carry buffer
     bool own_xch = true;
     unsigned* bar_d = nullptr;  // fused slab leaf grid barrier
+    cplx* mpscratch_d = nullptr;  // split K-branch history products
+    bool split_k = true;
     long long* dbgclk_d = nullptr;
     bool fused_leaf = true;
     // levels
@@ -532,6 +534,13 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             FT_CUDA(launch_spectra(p->col_d, N, (int)B, lv.n, lv.m, lv.K, p->J, p->spec_d + lv.spec_off,
                                    p->tw_d, p->logT, p->stream));
     }
+    {
+        bool needs = false;
+        for (auto& lv : p->levels) needs = needs || lv.K >= 8;
+        p->split_k = getenv("FT_CLUSTER_K") == nullptr;
+        if (needs && p->split_k)
+            if ((rc = alloc_copy((void**)&p->mpscratch_d, nullptr, kMpScratchBytes))) return rc;
+    }
     FT_CUDA(cudaStreamSynchronize(p->stream));
     *out = p;
     return FT_OK;
@@ -613,6 +622,9 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.logT = p->logT;
             a.col = p->col_d;
             a.J = p->J;
+            a.scratch = (lv.K >= 8 && p->split_k) ? p->mpscratch_d : nullptr;  // K = 4: clusters measured faster
+            a.pair_begin = 0;
+            a.pair_count = 0;
             FT_CUDA(launch_mp(a, lv.groups, st));
         }
         ++nl;
@@ -952,7 +964,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev0) cudaEventDestroy(p->ev0);

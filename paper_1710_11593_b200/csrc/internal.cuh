@@ -96,6 +96,8 @@ struct MpArgs {
     int logT;
     const double* col;         // [B][N] (near field)
     int J;                     // near-field lags summed exactly: 1..J-1
+    cplx* scratch;             // split K-branch levels: branch results [pairs][K][m]
+    int pair_begin, pair_count;  // split K-branch levels: pairs of this launch
 };
 
 struct DirectArgs {
@@ -131,6 +133,7 @@ struct SpecArgs;
 size_t mp_smem_bytes(int G, int m);
 bool mp_is_direct(int n);
 bool mp_is_single(int n);
+constexpr uint64_t kMpScratchBytes = 256ull << 20;  // split K-branch scratch (L2-sized batches)
 cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, int J, cplx* spec,
                                   const cplx* tw, cudaStream_t st);
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st);

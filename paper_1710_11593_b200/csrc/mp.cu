@@ -18,6 +18,8 @@
 // the GMRES fast paths (src/schemes.cpp:464-474, :353-369).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "fft.cuh"
 #include "internal.cuh"
 
@@ -59,18 +61,21 @@ __device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
     }
 }
 
-template <int K, int LOGM>
+// SPLIT = true: no cluster; CTA (b, pair) writes its branch result to
+// a.scratch and mpB_kernel performs the cross-branch combine (K >= 4 levels:
+// 16-CTA clusters packed badly -- 14 active clusters -- and stalled on
+// cluster barriers, ncu).
+template <int K, int LOGM, bool SPLIT>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
     __shared__ PairInfo s_pair[kMpTile / 32];
-    cg::cluster_group cluster = cg::this_cluster();
-    const int b = (int)cluster.block_rank();
+    const int b = SPLIT ? (int)blockIdx.x : (int)cg::this_cluster().block_rank();
     constexpr int m = 1 << LOGM, logm = LOGM;
     const int G = a.G, n = a.n;
     const int total = G * m;
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
-    const int pair0 = blockIdx.y * G;
+    const int pair0 = (SPLIT ? a.pair_begin : 0) + blockIdx.y * G;
     const uint64_t N = a.N;
 
     for (int g = threadIdx.x; g < G; g += blockDim.x) {
@@ -153,6 +158,12 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     __syncthreads();
     mid_inv<LOGM - 4, LOGM>(buf, total, a.tw);
     pass_c<16, LOGM, true>(buf, total, a.tw);  // last inverse pass (S = m) -> SMEM for the combine
+    if constexpr (SPLIT) {
+        cplx* out = a.scratch + ((uint64_t)(pair0 - a.pair_begin) * K + b) * m;
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) out[idx] = buf[sphys(idx)];
+        return;
+    } else {
+    cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
 
     // 3. inverse K-point DFT across the cluster's branches (DSMEM), near field, store.
@@ -236,6 +247,68 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
         }
     }
     cluster.sync();
+    }
+}
+
+// Cross-branch combine of the split K-branch levels: thread <-> (pair, r):
+// read the K branch values, untwist by w_n^(b r), K-point DFT, store the K/2
+// target outputs t = mid + (q - K/2) m + r (plus the exact near field).
+template <int K, int LOGM>
+__global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
+    constexpr int m = 1 << LOGM;
+    const int n = a.n;
+    const int pl = blockIdx.y;  // pair within the batch
+    const int rp = a.pair_begin + pl;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    if (rp >= npairs || r >= m) return;
+    const uint64_t N = a.N;
+    const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+    const int i1 = 2 * lp;
+    const bool has2 = i1 + 1 < a.nodes;
+    const uint64_t row1 = (uint64_t)(pb * a.nodes + i1);
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    double r1[K / 2], r2[K / 2];
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) {
+        const uint64_t t = a.mid + (uint64_t)q * m + r;
+        r1[q] = t < tend ? a.rsrc[row1 * N + t] : 0.0;
+        r2[q] = (t < tend && has2) ? a.rsrc[(row1 + 1) * N + t] : 0.0;
+    }
+    const cplx* in = a.scratch + (uint64_t)pl * K * m + r;
+    cplx wv[K];
+#pragma unroll
+    for (int bb = 0; bb < K; ++bb) wv[bb] = in[(uint64_t)bb * m];
+    const cplx w1 = ldgc(&a.tw[n + r]);  // w_n^r
+    cplx wp = w1;
+#pragma unroll
+    for (int bb = 1; bb < K; ++bb) {
+        wv[bb] = cmul(wv[bb], wp);
+        if (bb + 1 < K) wp = cmul(wp, w1);
+    }
+    dft_reg<K, false>(wv);
+#pragma unroll
+    for (int q = K / 2; q < K; ++q) {
+        const uint64_t t = a.mid + (uint64_t)(q - K / 2) * m + r;
+        if (t >= tend) continue;
+        cplx y = wv[q];
+        const int tp = (int)(t - a.mid);
+        if (tp < a.J - 1) {
+            const double* cp = a.col + (uint64_t)pb * N;
+            const double* x1 = a.X + row1 * N;
+            const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
+            double s1 = 0.0, s2 = 0.0;
+            for (uint64_t j = a.mid; j-- > jlo;) {
+                const double cv = cp[t - j];
+                s1 = fma(cv, x1[j], s1);
+                if (has2) s2 = fma(cv, x1[N + j], s2);
+            }
+            y.x += s1;
+            y.y += s2;
+        }
+        a.X[row1 * N + t] = r1[q - K / 2] - y.x;
+        if (has2) a.X[(row1 + 1) * N + t] = r2[q - K / 2] - y.y;
+    }
 }
 
 // ---- single-CTA n-point FFT history product (512 <= n <= 8192) -------------
@@ -546,12 +619,38 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
 size_t mp_smem_bytes(int G, int m) { return sizeof(cplx) * (size_t)spad_len(G * m); }
 
 template <int K, int LOGM>
-static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
+static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(mp_kernel<K, LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
-        if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr_set = true;
+    }
+    constexpr int m = 1 << LOGM;
+    const int npairs = (a0.rows / a0.nodes) * a0.pairs_per_problem;
+    const int batch = (int)std::max<uint64_t>(1, kMpScratchBytes / ((uint64_t)K * m * sizeof(cplx)));
+    MpArgs a = a0;
+    for (int p0 = 0; p0 < npairs; p0 += batch) {
+        a.pair_begin = p0;
+        a.pair_count = std::min(batch, npairs - p0);
+        mp_kernel<K, LOGM, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        mpB_kernel<K, LOGM><<<dim3(m / kMpThreads, a.pair_count), kMpThreads, 0, st>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+template <int K, int LOGM>
+static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
+    if (a.scratch) return launch_mp_split<K, LOGM>(a, st);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(mp_kernel<K, LOGM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
+        if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -566,7 +665,7 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mp_kernel<K, LOGM>, a);
+    return cudaLaunchKernelEx(&cfg, mp_kernel<K, LOGM, false>, a);
 }
 
 template <int H>
