@@ -88,6 +88,11 @@ __device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
 template <int R>
 __device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restrict__ tw, int S, int j) {
     w[0] = {1.0, 0.0};
+#ifdef FT_TW_DIRECT
+    // direct lookups w_S^{qj} = tw[S + qj] (qj < S): no product chain, exact table values
+#pragma unroll
+    for (int q = 1; q < R; ++q) w[q] = ldgc(&tw[S + q * j]);
+#else
     if (R >= 2) w[1] = ldgc(&tw[S + j]);
     if (R >= 4) {
         w[2] = ldgc(&tw[(S >> 1) + j]);
@@ -103,6 +108,7 @@ __device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restri
 #pragma unroll
         for (int q = 9; q < 16; ++q) w[q] = cmul(w[8], w[q - 8]);
     }
+#endif
 }
 
 // R-point forward DFT (natural order in/out) of R/2 data points followed by R/2

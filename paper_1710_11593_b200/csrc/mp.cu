@@ -322,15 +322,107 @@ __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
 //     writes R := R - y straight to HBM.
 // The spectrum (spec1_kernel) uses the same pass plan, so digit-reversed
 // orders agree.
+// Mid passes, each preceded by its barrier, so callers can issue the next
+// phase's global loads (spectrum, twiddles, targets) before the final barrier.
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_fwd_s(cplx* buf, int total, const cplx* tw) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        __syncthreads();
+        pass_c<16, LOGS, false>(buf, total, tw);
+        mid_fwd_s<LOGS - 4, LOGN>(buf, total, tw);
+    }
+}
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_inv_s(cplx* buf, int total, const cplx* tw) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        mid_inv_s<LOGS - 4, LOGN>(buf, total, tw);
+        __syncthreads();
+        pass_c<16, LOGS, true>(buf, total, tw);
+    }
+}
+
+// Last inverse pass (S = n, radix 16) inputs of task t: twiddles and the
+// targets' right-hand sides (outputs p >= 8 are the targets [mid, mid + h)).
+template <int Q0>
+__device__ __forceinline__ void mp1_last_prefetch(const MpArgs& a, const PairInfo* s_pair, int pair0, int npairs,
+                                                  int t, cplx (&w)[16], double (&r1)[8], double (&r2)[8]) {
+    const int g = t / Q0, j = t - g * Q0;
+    const PairInfo pi = s_pair[g];
+    const bool live = pair0 + g < npairs;
+    const uint64_t tend = a.hi < a.N ? a.hi : a.N;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
+        const bool ok = live && tt < tend;
+        r1[p] = ok ? a.rsrc[pi.row1 * a.N + tt] : 0.0;
+        r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * a.N + tt] : 0.0;
+    }
+    pass_twiddles<16>(w, a.tw, Q0 * 16, j);
+}
+
+template <int Q0>
+__device__ __forceinline__ void mp1_last_task(const MpArgs& a, cplx* buf, const PairInfo* s_pair, int pair0,
+                                              int npairs, int t, const cplx (&w)[16], const double (&r1)[8],
+                                              const double (&r2)[8]) {
+    constexpr int n = Q0 * 16;
+    const int g = t / Q0, j = t - g * Q0;
+    const PairInfo pi = s_pair[g];
+    const uint64_t N = a.N;
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    const int pbx = sphys(g * n + j);
+    cplx v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = buf[pbx + q * (Q0 + (Q0 >> 4))];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) v[q] = cmulc(v[q], w[q]);
+    dft_reg<16, true>(v);
+    if (pair0 + g >= npairs) return;
+#pragma unroll
+    for (int p = 8; p < 16; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)(p - 8) * Q0;
+        if (tt >= tend) continue;
+        cplx y = v[p];
+        const int tp = (int)(tt - a.mid);
+        if (tp < a.J - 1) {  // exact near field: lags t - j < J
+            const double* cp = a.col + (uint64_t)pi.pb * N;
+            const double* xr = a.X + pi.row1 * N;
+            const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
+            double s1 = 0.0, s2 = 0.0;
+            for (uint64_t jj = a.mid; jj-- > jlo;) {
+                const double cv = cp[tt - jj];
+                s1 = fma(cv, xr[jj], s1);
+                if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
+            }
+            y.x += s1;
+            y.y += s2;
+        }
+        a.X[pi.row1 * N + tt] = r1[p - 8] - y.x;
+        if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 8] - y.y;
+    }
+}
+
+// G = kMpTile / n row pairs per CTA (compile time; pairs past the end are
+// dead).  When a CTA holds exactly 16 points per thread (n <= kMpTile), each
+// phase's global loads -- spectrum for the fused pass, twiddles and targets for
+// the last pass -- are issued before the barrier that precedes the phase
+// (ncu: these L1/L2 round trips were the top long-scoreboard stalls).
 template <int LOGN>
-__global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
+#ifndef FT_MP1_MINB
+#define FT_MP1_MINB 2
+#endif
+__global__ void __launch_bounds__(kMpThreads, FT_MP1_MINB) mp1_kernel(MpArgs a) {
     using PL = Plan1<LOGN>;
-    constexpr int n = PL::n, h = PL::h, Q0 = PL::Q0, RL = PL::RL;
+    constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
+    constexpr int G = n >= kMpTile ? 1 : kMpTile / n;
+    constexpr int total = G * n;
+#ifdef FT_MP1_NOPRE
+    constexpr bool PRE = false;
+#else
+    constexpr bool PRE = total == kMpThreads * 16;
+#endif
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
-    __shared__ PairInfo s_pair[kMpTile / 256];
-    const int G = a.G;
-    const int total = G * n;
+    __shared__ PairInfo s_pair[G];
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
     const int pair0 = blockIdx.x * G;
     const uint64_t N = a.N;
@@ -343,12 +435,14 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
     __syncthreads();
 
     // pass 0 (S = n, radix 16) from HBM; inputs p >= 8 are the zero padding
-    for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
+#pragma unroll 1
+    for (int t = threadIdx.x; t < total / 16; t += kMpThreads) {
         const int g = t / Q0, j = t - g * Q0;
         const PairInfo pi = s_pair[g];
         const double* x1 = a.X + pi.row1 * N + a.lo + j;
         const bool live = pair0 + g < npairs;
         cplx v[16];
+#pragma unroll
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
             v[p].x = live ? x1[(uint64_t)p * Q0] : 0.0;
@@ -363,74 +457,68 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1_kernel(MpArgs a) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) buf[pb + q * (Q0 + (Q0 >> 4))] = v[q];
     }
-    __syncthreads();
-    mid_fwd<LOGN - 4, LOGN>(buf, total, a.tw);
+    mid_fwd_s<LOGN - 4, LOGN>(buf, total, a.tw);
 
     // fused: last forward pass (S = RL, twiddle-free), spectrum, first inverse pass
-    for (int t = threadIdx.x; t < total / RL; t += blockDim.x) {
-        const int base = t * RL;
-        const int g = base >> LOGN;
-        const int pbx = sphys(base);
-        cplx v[RL];
+    constexpr int FT = total / RL / kMpThreads;  // fused tasks per thread (PRE)
+    cplx spv[PRE ? 16 : 1];
+    if constexpr (PRE) {
 #pragma unroll
-        for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
-        dft_reg<RL, false>(v);
-        const cplx* sp = a.spec + (uint64_t)s_pair[g].pb * n + (base & (n - 1));
+        for (int k = 0; k < FT; ++k) {
+            const int base = (threadIdx.x + k * kMpThreads) * RL;
+            const cplx* sp = a.spec + (uint64_t)s_pair[base >> LOGN].pb * n + (base & (n - 1));
 #pragma unroll
-        for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], ldgc(&sp[p]));
-        dft_reg<RL, true>(v);
-#pragma unroll
-        for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+            for (int p = 0; p < RL; ++p) spv[k * RL + p] = ldgc(&sp[p]);
+        }
     }
     __syncthreads();
-    mid_inv<LOGN - 4, LOGN>(buf, total, a.tw);
+    if constexpr (PRE) {
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+            const int pbx = sphys((threadIdx.x + k * kMpThreads) * RL);
+            cplx v[RL];
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+            dft_reg<RL, false>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], spv[k * RL + p]);
+            dft_reg<RL, true>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+        }
+    } else {
+        for (int t = threadIdx.x; t < total / RL; t += kMpThreads) {
+            const int base = t * RL;
+            const int pbx = sphys(base);
+            cplx v[RL];
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+            dft_reg<RL, false>(v);
+            const cplx* sp = a.spec + (uint64_t)s_pair[base >> LOGN].pb * n + (base & (n - 1));
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], ldgc(&sp[p]));
+            dft_reg<RL, true>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+        }
+    }
+    mid_inv_s<LOGN - 4, LOGN>(buf, total, a.tw);
 
     // last inverse pass (S = n, radix 16): outputs p >= 8 are the targets [mid, mid + h)
-    const uint64_t tend = a.hi < N ? a.hi : N;
-    for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
-        const int g = t / Q0, j = t - g * Q0;
-        const PairInfo pi = s_pair[g];
-        const bool live = pair0 + g < npairs;
-        // prefetch the targets' right-hand sides
-        double r1[8], r2[8];
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
-            const bool ok = live && tt < tend;
-            r1[p] = ok ? a.rsrc[pi.row1 * N + tt] : 0.0;
-            r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
-        }
-        const int pbx = sphys(g * n + j);
-        cplx v[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = buf[pbx + q * (Q0 + (Q0 >> 4))];
+    if constexpr (PRE) {
         cplx w[16];
-        pass_twiddles<16>(w, a.tw, n, j);
-#pragma unroll
-        for (int q = 1; q < 16; ++q) v[q] = cmulc(v[q], w[q]);
-        dft_reg<16, true>(v);
-        if (!live) continue;
-#pragma unroll
-        for (int p = 8; p < 16; ++p) {
-            const uint64_t tt = a.mid + j + (uint64_t)(p - 8) * Q0;
-            if (tt >= tend) continue;
-            cplx y = v[p];
-            const int tp = (int)(tt - a.mid);
-            if (tp < a.J - 1) {  // exact near field: lags t - j < J
-                const double* cp = a.col + (uint64_t)pi.pb * N;
-                const double* xr = a.X + pi.row1 * N;
-                const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
-                double s1 = 0.0, s2 = 0.0;
-                for (uint64_t jj = a.mid; jj-- > jlo;) {
-                    const double cv = cp[tt - jj];
-                    s1 = fma(cv, xr[jj], s1);
-                    if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
-                }
-                y.x += s1;
-                y.y += s2;
-            }
-            a.X[pi.row1 * N + tt] = r1[p - 8] - y.x;
-            if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 8] - y.y;
+        double r1[8], r2[8];
+        mp1_last_prefetch<Q0>(a, s_pair, pair0, npairs, threadIdx.x, w, r1, r2);
+        __syncthreads();
+        mp1_last_task<Q0>(a, buf, s_pair, pair0, npairs, threadIdx.x, w, r1, r2);
+    } else {
+        __syncthreads();
+#pragma unroll 1
+        for (int t = threadIdx.x; t < total / 16; t += kMpThreads) {
+            cplx w[16];
+            double r1[8], r2[8];
+            mp1_last_prefetch<Q0>(a, s_pair, pair0, npairs, t, w, r1, r2);
+            mp1_last_task<Q0>(a, buf, s_pair, pair0, npairs, t, w, r1, r2);
         }
     }
 }
@@ -688,15 +776,15 @@ bool mp_is_single(int n) { return !mp_is_direct(n) && n >= 256 && n <= kMpSingle
 template <int LOGN>
 static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
     constexpr int n = 1 << LOGN;
-    const size_t smem = mp_smem_bytes(a.G, n);
+    constexpr int G = n >= kMpTile ? 1 : kMpTile / n;  // as in mp1_kernel
+    const size_t smem = mp_smem_bytes(G, n);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(mp1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mp_smem_bytes(1, n > kMpTile ? n : kMpTile));
+        cudaFuncSetAttribute(mp1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
-    const int ctas = (npairs + a.G - 1) / a.G;
+    const int ctas = (npairs + G - 1) / G;
     mp1_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
