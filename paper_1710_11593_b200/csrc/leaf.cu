@@ -496,12 +496,17 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
             }
             if (a.dbg & 8) continue;  // timing ablation only (wrong results)
 #pragma unroll
-            for (int i = 0; i + 1 < L; ++i) {
-                const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
-                accF[i] = fma(hF.x, EL, fma(hF.y, ER, accF[i + 1]));
-                if (TRI) {
-                    const double2 hB = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][2]);
-                    accB[i] = fma(hB.x, EL, fma(hB.y, ER, accB[i + 1]));
+            for (int c = 0; c < L; c += 8) {
+                if (c == 0 || k + 1 + c < len) {  // dead entries (k + 1 + i >= len) skipped in chunks
+#pragma unroll
+                    for (int i = c; i < c + 8 && i + 1 < L; ++i) {
+                        const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
+                        accF[i] = fma(hF.x, EL, fma(hF.y, ER, accF[i + 1]));
+                        if (TRI) {
+                            const double2 hB = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][2]);
+                            accB[i] = fma(hB.x, EL, fma(hB.y, ER, accB[i + 1]));
+                        }
+                    }
                 }
             }
             accF[L - 1] = 0.0;

@@ -777,7 +777,10 @@ template <int LOGN>
 static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
     constexpr int n = 1 << LOGN;
     constexpr int G = n >= kMpTile ? 1 : kMpTile / n;  // as in mp1_kernel
-    const size_t smem = mp_smem_bytes(G, n);
+#ifndef FT_MP1_SMEM_PAD
+#define FT_MP1_SMEM_PAD 0
+#endif
+    const size_t smem = mp_smem_bytes(G, n) + FT_MP1_SMEM_PAD;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(mp1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
