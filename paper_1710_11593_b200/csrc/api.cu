@@ -4,6 +4,7 @@
 // divide-and-conquer driver.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -106,6 +107,9 @@ struct ft_plan {
     double* den_d = nullptr;
     double* scratch_d = nullptr;  // [B][nodes]
     double* work_d = nullptr;     // staging for host buffers
+    double* rdev_d = nullptr;     // streamed host solves: device copy of the caller's R
+    cudaStream_t h2d_st = nullptr, d2h_st = nullptr;  // streamed host solves: copy engines
+    std::vector<cudaEvent_t> h2d_ev, d2h_ev;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -296,6 +300,15 @@ int alloc_copy(void** dst, const void* src, size_t bytes) {
     FT_CUDA(cudaMalloc(dst, bytes ? bytes : 8));
     if (bytes && src) FT_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
     return FT_OK;
+}
+
+bool is_pinned_host(const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
 }
 
 bool is_device_ptr(const void* ptr) {
@@ -546,8 +559,21 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     return FT_OK;
 }
 
+// Streamed host solve: the caller's R arrives in time chunks of C steps on a
+// copy stream and is added by the leaf that solves those steps (history
+// products accumulate into a zeroed X, linear in R); finished chunks of U
+// leave on a second copy stream as soon as their last leaf is done.  PCIe
+// traffic in both directions overlaps the solve.
+struct StreamIO {
+    uint64_t C = 0;               // chunk steps (multiple of the leaf length)
+    bool defer = false;           // R streamed into rdev (leaves add it)
+    const double* rdev = nullptr;
+    double* u_host = nullptr;     // non-null: stream U chunks back
+    uint64_t waited = 0;          // H2D chunks the compute stream has waited for
+};
+
 int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
-             std::vector<cudaEvent_t>* evs = nullptr) {
+             std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
     // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve)
@@ -561,7 +587,16 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
         if (op.kind == OP_LEAF) {
             LeafArgs a;
             a.X = X;
-            a.src = op.first ? rhs : X;
+            const bool defer = io && io->defer;
+            a.src = (op.first && !defer) ? rhs : X;
+            a.radd = defer ? io->rdev : nullptr;
+            if (defer) {  // this leaf's R chunk must have landed
+                const uint64_t c = op.t0 / io->C;
+                if (c >= io->waited) {
+                    FT_CUDA(cudaStreamWaitEvent(st, p->h2d_ev[c], 0));
+                    io->waited = c + 1;
+                }
+            }
             a.N = N;
             a.t0 = op.t0;
             a.len = op.len;
@@ -601,11 +636,21 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
                 FT_CUDA(launch_leaf_correct(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
                 ++nl;
             }
+            if (io && io->u_host) {  // a finished chunk of U goes back while the solve continues
+                const uint64_t end = op.t0 + (uint64_t)op.len;
+                if (end % io->C == 0 || end == N) {
+                    const uint64_t c = (end - 1) / io->C, c0 = c * io->C, w = end - c0;
+                    FT_CUDA(cudaEventRecord(p->d2h_ev[c], st));
+                    FT_CUDA(cudaStreamWaitEvent(p->d2h_st, p->d2h_ev[c], 0));
+                    FT_CUDA(cudaMemcpy2DAsync(io->u_host + c0, sizeof(double) * N, X + c0, sizeof(double) * N,
+                                              sizeof(double) * w, rows_of(p), cudaMemcpyDeviceToHost, p->d2h_st));
+                }
+            }
         } else {
             const Level& lv = p->levels[op.level];
             MpArgs a;
             a.X = X;
-            a.rsrc = op.first ? rhs : X;
+            a.rsrc = (op.first && !(io && io->defer)) ? rhs : X;
             a.N = N;
             a.lo = op.t0;
             a.mid = op.mid;
@@ -807,6 +852,73 @@ int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const d
     return FT_OK;
 }
 
+// Fast solve with pinned host buffers: chunked H2D of R and D2H of U overlap
+// the solve (StreamIO).  Pageable host buffers take the serial path below.
+static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool stream_rhs,
+                          std::chrono::steady_clock::time_point t_start) {
+    const uint64_t N = p->N, rows = rows_of(p);
+    const size_t bytes = sizeof(double) * rows * N;
+    const cudaStream_t st = p->stream;
+    const bool u_dev = is_device_ptr(u);
+    double* X = u;
+    if (!u_dev) {
+        int rc = ensure_work(p);
+        if (rc) return rc;
+        X = p->work_d;
+    }
+    StreamIO io;
+    // chunk: wide enough for efficient 2D DMA rows, small enough for a short fill/drain
+    uint64_t C = getenv("FT_STREAM_CHUNK") ? (uint64_t)atoll(getenv("FT_STREAM_CHUNK")) : 2048;  // B200 PCIe: 16 KB rows best (measured 256..4096)
+    C = std::max<uint64_t>((C + p->L - 1) / p->L * p->L, (uint64_t)p->L);
+    io.C = std::min<uint64_t>(N, C);
+    const uint64_t nch = (N + io.C - 1) / io.C;
+    if (!p->h2d_st) {
+        FT_CUDA(cudaStreamCreateWithFlags(&p->h2d_st, cudaStreamNonBlocking));
+        FT_CUDA(cudaStreamCreateWithFlags(&p->d2h_st, cudaStreamNonBlocking));
+    }
+    while (p->h2d_ev.size() < nch) {
+        cudaEvent_t e1, e2;
+        FT_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        FT_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        p->h2d_ev.push_back(e1);
+        p->d2h_ev.push_back(e2);
+    }
+    FT_CUDA(cudaEventRecord(p->ev0, st));
+    const double* src = rhs;
+    if (stream_rhs) {
+        if (!p->rdev_d) FT_CUDA(cudaMalloc(&p->rdev_d, bytes));
+        io.defer = true;
+        io.rdev = p->rdev_d;
+        src = X;
+        FT_CUDA(cudaStreamWaitEvent(p->h2d_st, p->ev0, 0));  // previous solves on this plan are done
+        for (uint64_t c = 0; c < nch; ++c) {
+            const uint64_t c0 = c * io.C, w = std::min<uint64_t>(N, c0 + io.C) - c0;
+            FT_CUDA(cudaMemcpy2DAsync(p->rdev_d + c0, sizeof(double) * N, rhs + c0, sizeof(double) * N,
+                                      sizeof(double) * w, rows, cudaMemcpyHostToDevice, p->h2d_st));
+            FT_CUDA(cudaEventRecord(p->h2d_ev[c], p->h2d_st));
+        }
+        FT_CUDA(cudaMemsetAsync(X, 0, bytes, st));  // history accumulates into zero; leaves add R
+    }
+    io.u_host = u_dev ? nullptr : u;
+    uint64_t launches = 0;
+    int rc = run_fast(p, X, src, &launches, nullptr, &io);
+    if (rc) return rc;
+    FT_CUDA(cudaEventRecord(p->ev1, st));
+    FT_CUDA(cudaStreamSynchronize(st));
+    if (!u_dev) FT_CUDA(cudaStreamSynchronize(p->d2h_st));
+    float ms = 0.f;
+    FT_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    if (rep) {
+        std::snprintf(rep->method, sizeof(rep->method), "%s", "fast");
+        rep->iterations = 0;
+        rep->residual = 0.0;
+        rep->device_ms = ms;
+        rep->kernel_launches = launches;
+        rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+    return FT_OK;
+}
+
 static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool fast) {
     if (!p || !rhs || !u) return set_err(FT_EINVAL, "ft_solve: null argument");
     if (!fast && p->part_world > 1) return set_err(FT_EINVAL, "ft_solve_direct: not available on partitioned plans");
@@ -816,6 +928,9 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     const size_t bytes = sizeof(double) * elems;
     const bool rhs_dev = is_device_ptr(rhs), u_dev = is_device_ptr(u);
     const cudaStream_t st = p->stream;
+    const bool stream_rhs = fast && !rhs_dev && is_pinned_host(rhs);
+    const bool stream_u = fast && !u_dev && is_pinned_host(u);
+    if ((stream_rhs || stream_u) && !getenv("FT_NO_STREAM")) return solve_streamed(p, rhs, u, rep, stream_rhs, t_start);
     double* X;
     const double* src;
     if (u_dev) {
@@ -967,6 +1082,11 @@ void ft_destroy(ft_plan* p) {
                     p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
+    if (p->rdev_d) cudaFree(p->rdev_d);
+    for (cudaEvent_t e : p->h2d_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->d2h_ev) cudaEventDestroy(e);
+    if (p->h2d_st) cudaStreamDestroy(p->h2d_st);
+    if (p->d2h_st) cudaStreamDestroy(p->d2h_st);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);

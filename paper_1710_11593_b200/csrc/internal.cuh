@@ -58,6 +58,7 @@ __host__ __device__ inline cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - 
 struct LeafArgs {
     double* X;                 // rows x N, node-major (U for solved steps, R after)
     const double* src;         // where this leaf's R tile is read from (X or the caller's rhs)
+    const double* radd;        // streamed host solves: R added at staging (history in src), else null
     uint64_t N;                // row pitch = time steps
     uint64_t t0;               // first step of the leaf
     int len;                   // steps in this leaf (<= L)

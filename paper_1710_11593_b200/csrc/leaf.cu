@@ -62,9 +62,11 @@ __device__ __forceinline__ void scan_consts(ScanConsts<NPT>& sc, const double* l
 
 // dst[q][k] (row stride L+1) = src[(row0 + q) * N + t0 + k] for q < rows, k < len;
 // consecutive threads read consecutive steps of a node row, 8 loads in flight.
+// radd (optional, same layout as src): added element-wise -- the streamed host
+// path keeps the caller's R out of X until the leaf that solves those steps.
 template <int L>
-__device__ __forceinline__ void stage_rows(double* dst, const double* src, uint64_t row0, uint64_t N,
-                                           uint64_t t0, int rows, int len) {
+__device__ __forceinline__ void stage_rows(double* dst, const double* src, const double* radd, uint64_t row0,
+                                           uint64_t N, uint64_t t0, int rows, int len) {
     // 16-byte loads when rows are 16-byte aligned and whole (the common case:
     // even N, full leaf); 8 double2 in flight per thread
     if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
@@ -78,6 +80,18 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, uint6
                 const int q = e / HL, k2 = e - q * HL;
                 v[u] = e < total ? __ldcg(reinterpret_cast<const double2*>(src + (row0 + q) * N + t0) + k2)
                                  : make_double2(0.0, 0.0);
+            }
+            if (radd) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * kLeafThreads + threadIdx.x;
+                    const int q = e / HL, k2 = e - q * HL;
+                    if (e < total) {
+                        const double2 r = __ldcs(reinterpret_cast<const double2*>(radd + (row0 + q) * N + t0) + k2);
+                        v[u].x += r.x;
+                        v[u].y += r.y;
+                    }
+                }
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -98,7 +112,7 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, uint6
         for (int u = 0; u < 8; ++u) {
             const int e = e0 + u * kLeafThreads + threadIdx.x;
             const int q = e / len, k = e - q * len;
-            v[u] = e < total ? src[(row0 + q) * N + t0 + k] : 0.0;
+            v[u] = e < total ? src[(row0 + q) * N + t0 + k] + (radd ? radd[(row0 + q) * N + t0 + k] : 0.0) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -229,7 +243,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     if (stamp) a.dbg_clk[8] = clock64();
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
-    stage_rows<L>(s_out, a.src, rowb, N, a.t0, mreal, len);
+    stage_rows<L>(s_out, a.src, a.radd, rowb, N, a.t0, mreal, len);
     __syncthreads();
     double tile[NPT][L];
 #pragma unroll

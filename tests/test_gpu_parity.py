@@ -204,3 +204,42 @@ def test_in_place_and_device_buffers(ft, oracle_mod):
     assert np.array_equal(Rd.cpu().numpy(), R)  # input untouched
     plan.solve_fast(Rd, Rd)
     assert np.array_equal(Rd.cpu().numpy(), U)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,kw", [(4, dict(time_steps=4500, cells=4097)), (2, dict(time_steps=16384)),
+                                    (3, dict(time_steps=5000, cells=65)), (5, dict(time_steps=3000))])
+def test_streamed_host_solve(ft, oracle_mod, cid, kw):
+    """Pinned host buffers take the streamed path (chunked H2D of R added by the
+    leaves, D2H of finished chunks overlapping the solve); it must agree with the
+    device-buffer solve to rounding and with the oracle, for host->host,
+    host->device, device->host and in-place host solves."""
+    import torch
+
+    w = W.config(cid, **kw)
+    plan = ft.Plan(w.specs)
+    Rd = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.assemble_rhs_modes(Rd, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    Ud = torch.empty_like(Rd)
+    plan.solve_fast(Rd, Ud)
+    U0 = Ud.cpu().numpy()
+    scale = np.max(np.abs(U0))
+    hR = torch.empty(plan.shape, dtype=torch.float64, pin_memory=True)
+    hR.copy_(Rd.cpu())
+    hU = torch.empty(plan.shape, dtype=torch.float64, pin_memory=True)
+    for _ in range(2):  # second solve reuses the plan's staging and events
+        hU.zero_()
+        plan.solve_fast(hR.numpy(), hU.numpy())
+        assert np.max(np.abs(hU.numpy() - U0)) <= 1e-12 * scale
+    Ud2 = torch.zeros_like(Rd)
+    plan.solve_fast(hR.numpy(), Ud2)  # host -> device
+    assert np.max(np.abs(Ud2.cpu().numpy() - U0)) <= 1e-12 * scale
+    hU.zero_()
+    plan.solve_fast(Rd, hU.numpy())  # device -> host (first touch from the device rhs)
+    assert np.array_equal(hU.numpy(), U0)
+    hI = hR.clone().pin_memory()
+    plan.solve_fast(hI.numpy(), hI.numpy())  # in place on pinned host memory
+    assert np.max(np.abs(hI.numpy() - U0)) <= 1e-12 * scale
+    if w.N * w.nodes * w.B <= 3_000_000:
+        F, u0, phi = _inputs(oracle_mod, w)
+        assert oracle_mod.relerr(hU.numpy(), oracle_mod.direct(w, F, u0, phi)) <= 1e-10
