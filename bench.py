@@ -39,6 +39,17 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+# DRAM bytes / algorithmic bytes of one history-product launch, measured with
+# ncu --set full on B200 (profiles/ncu_r01/README.md): direct kernel (n <= 128),
+# single-CTA FFT kernel (256 <= n <= 8192), 4-CTA cluster (n = 16384), split
+# A + B kernels with the branch scratch round trip (n >= 32768).
+NCU_DRAM_OVER_ALG = {"direct": 0.67, "single": 0.80, "cluster": 1.00, "split": 2.27}
+
+
+def mp_family(n: int) -> str:
+    return "direct" if n <= 128 else "single" if n <= 8192 else "cluster" if n <= 16384 else "split"
+
+
 def bytes_per_unknown(N: int) -> float:
     """B_alg = 8 B M N (1.5 D + 2), D = log2(N/64)."""
     D = max(0.0, math.log2(N / 64))
@@ -280,6 +291,15 @@ def run_ours(args, world, rank, local):
     dom = "mp_kernel" if mp_ms >= lf_ms else "leaf_kernel"
     d_ms, d_bytes, d_n = (mp_ms, mp_bytes, len(mp)) if dom == "mp_kernel" else (lf_ms, lf_bytes, len(lf))
     achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
+    # DRAM traffic per launch of the dominant kernel: each level's algorithmic
+    # bytes scaled by the ncu-measured DRAM/algorithmic ratio of its kernel family
+    traffic, traffic_note = None, None
+    if dom == "mp_kernel" and d_n:
+        leaf_len = int(plan.info.leaf)
+        dram = sum(o["bytes"] * NCU_DRAM_OVER_ALG[mp_family(2 * leaf_len << o["level"])] for o in mp)
+        traffic = dram / d_n
+        traffic_note = ("bytes per launch (DRAM read+write), per-level ncu ratios " + json.dumps(NCU_DRAM_OVER_ALG)
+                        + f"; algorithmic bytes per launch {d_bytes / d_n:.4g}")
     per_level = {}
     for o in mp:
         lv = per_level.setdefault(o["level"], {"launches": 0, "ms": 0.0, "bytes": 0})
@@ -331,7 +351,7 @@ def run_ours(args, world, rank, local):
             "hbm_roofline": {"bytes_per_unknown": bpu, "achieved_gbs_per_gpu": solve_gbs, "peak_gbs": hbm,
                              "frac": solve_gbs / hbm, "peak_kind": pk_kind},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "launches": d_n,
+                         "frac": achieved / hbm, "traffic": traffic, "traffic_note": traffic_note, "launches": d_n,
                          "kernel_ms_per_solve": d_ms, "peak_kind": pk_kind},
             "time_split_ms": {"mp_kernel": mp_ms, "leaf_kernel": lf_ms,
                               "mp_gbs": mp_bytes / (mp_ms / 1e3) / 1e9 if mp_ms else None,
