@@ -110,6 +110,11 @@ struct ft_plan {
     double* rdev_d = nullptr;     // streamed host solves: device copy of the caller's R
     cudaStream_t h2d_st = nullptr, d2h_st = nullptr;  // streamed host solves: copy engines
     std::vector<cudaEvent_t> h2d_ev, d2h_ev;
+    // CUDA graph of the whole launch schedule (device buffers, single rank), keyed by buffers
+    cudaGraphExec_t graph = nullptr;
+    const void* graph_X = nullptr;
+    const void* graph_src = nullptr;
+    uint64_t graph_launches = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -576,8 +581,11 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
              std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
-    // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve)
-    FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
+    // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve;
+    // a captured graph gets them from its launcher)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    FT_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap == cudaStreamCaptureStatusNone) FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     uint64_t nl = 0;
     unsigned leaf_index = 0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
@@ -955,8 +963,36 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     uint64_t launches = 0;
     FT_CUDA(cudaEventRecord(p->ev0, st));
     if (fast) {
-        int rc = run_fast(p, X, src, &launches);
-        if (rc) return rc;
+        const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH") && !(p->multi && p->fused_leaf);
+        if (use_graph) {
+            if (!p->graph || p->graph_X != X || p->graph_src != src) {
+                if (p->graph) cudaGraphExecDestroy(p->graph);
+                p->graph = nullptr;
+                cudaStream_t cs;
+                FT_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+                FT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+                const cudaStream_t keep = p->stream;
+                p->stream = cs;
+                int rc = run_fast(p, X, src, &p->graph_launches);
+                p->stream = keep;
+                cudaGraph_t g = nullptr;
+                const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+                cudaStreamDestroy(cs);
+                if (rc) return rc;
+                FT_CUDA(ce);
+                const cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+                cudaGraphDestroy(g);
+                FT_CUDA(ie);
+                p->graph_X = X;
+                p->graph_src = src;
+            }
+            FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
+            FT_CUDA(cudaGraphLaunch(p->graph, st));
+            launches = p->graph_launches;
+        } else {
+            int rc = run_fast(p, X, src, &launches);
+            if (rc) return rc;
+        }
     } else {
         if (src != X) FT_CUDA(cudaMemcpyAsync(X, src, bytes, cudaMemcpyDeviceToDevice, st));
         DirectArgs da;
@@ -1082,6 +1118,7 @@ void ft_destroy(ft_plan* p) {
                     p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
+    if (p->graph) cudaGraphExecDestroy(p->graph);
     if (p->rdev_d) cudaFree(p->rdev_d);
     for (cudaEvent_t e : p->h2d_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : p->d2h_ev) cudaEventDestroy(e);
