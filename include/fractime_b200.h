@@ -20,6 +20,14 @@
  *   ft_solve_fast              <- solve(spec, SolveMethod::Fast)    src/schemes.cpp:464-474, :353-369
  *                                 (GMRES + FFT matvec, src/krylov.cpp:107-223, replaced by a
  *                                 time-axis divide-and-conquer; same system, same answer)
+ *   ft_setup_toeplitz          <- ToeplitzOperator::lower_triangular() include/fractime/toeplitz.hpp:33
+ *                                 + lower_toeplitz_forward_solve()  src/toeplitz.cpp:169-186
+ *                                 (solved by the same D&C in O(n log^2 n); ft_solve_direct keeps
+ *                                 the reference's O(n^2) substitution order)
+ *   ft_toeplitz_matvec         <- embed_circulant() + toeplitz_matvec() src/toeplitz.cpp:84-115
+ *                                 (make_toeplitz_operator, src/toeplitz.cpp:198-201)
+ *   ft_block_matvec            <- BlockTridiagonalToeplitzOperator + block_matvec()
+ *                                 src/toeplitz.cpp:117-167 (make_block_operator :203-208)
  *   ft_last_error              <- the what() of the reference's std::exception
  *
  * Conventions
@@ -181,6 +189,33 @@ int ft_profile_fast(ft_plan* plan, const double* rhs_device, double* u_device, f
  * every (source, target) pair of the Toeplitz history exactly once. */
 int ft_schedule(uint64_t time_steps, uint64_t leaf, ft_op_time* out, uint64_t capacity,
                 uint64_t* count);
+
+/* Lower-triangular Toeplitz systems T_b x_b = r_b, b < count (ToeplitzOperator::
+ * lower_triangular + lower_toeplitz_forward_solve, src/toeplitz.cpp:169-186):
+ * first_cols[count][n] (host).  The plan solves with ft_solve_fast (the D&C,
+ * one "node") or ft_solve_direct (the reference's forward substitution, same
+ * summation order); buffers are [count][n].  col[0] == 0 fails with FT_ESOLVER
+ * "lower_toeplitz_forward_solve: zero diagonal" like the reference.  The
+ * ft_assemble_rhs* calls are rejected on such plans (no scheme). */
+int ft_setup_toeplitz(const double* first_cols, uint64_t n, uint64_t count, const ft_options* options,
+                      ft_plan** out);
+
+/* y[b] = T x[b], b < count, T the n x n Toeplitz matrix with T(i,j) =
+ * first_row[j-i] (j >= i) and first_col[i-j] (i > j); first_row == NULL means
+ * lower triangular.  Replaces embed_circulant + toeplitz_matvec
+ * (src/toeplitz.cpp:84-115); computed as a direct fp64 product on the GPU (no
+ * circulant rounding).  first_col[0] != first_row[0] -> FT_EINVAL with the
+ * reference's message (src/toeplitz.cpp:31-32).  All arrays host or device;
+ * x == y allowed. */
+int ft_toeplitz_matvec(const double* first_col, const double* first_row, uint64_t n, uint64_t count,
+                       const double* x, double* y);
+
+/* Block tridiagonal operator of m_blocks identical n x n Toeplitz diagonal
+ * blocks and off_scale * I off-diagonal blocks (BlockTridiagonalToeplitzOperator
+ * + block_matvec, src/toeplitz.cpp:117-167): y_b = T x_b + off_scale (x_{b-1} +
+ * x_{b+1}), added left then right as the reference does.  x, y: [m_blocks][n]. */
+int ft_block_matvec(const double* first_col, const double* first_row, uint64_t n, uint64_t m_blocks,
+                    double off_scale, const double* x, double* y);
 
 int ft_set_stream(ft_plan* plan, void* cuda_stream);
 const char* ft_last_error(void);

@@ -54,6 +54,10 @@ def olib():
         L.or_rhs_ode.argtypes = [D, U, D, P, D, P]
         L.or_forward_solve.argtypes = [P, P, U, P]
         L.or_forward_solve.restype = I
+        L.or_toeplitz_matvec.argtypes = [P, P, U, P, P]
+        L.or_toeplitz_matvec.restype = None
+        L.or_block_matvec.argtypes = [P, P, U, U, D, P, P]
+        L.or_block_matvec.restype = None
         L.or_direct_s4.argtypes = [D, U, U, D, D, P, P, P]
         L.or_direct_s3.argtypes = [D, U, U, D, D, P, P, P, I, P]
         L.or_march_ld.argtypes = [I, U, U, P, D, P, P]
@@ -85,6 +89,8 @@ def rlib():
         L.ref_ode_column.argtypes = [D, U, D, P]
         L.ref_forward_solve.argtypes = [P, P, U, P]
         L.ref_toeplitz_gmres.argtypes = [P, P, U, D, U, P, C.POINTER(U)]
+        L.ref_toeplitz_matvec.argtypes = [P, P, U, P, P]
+        L.ref_block_matvec.argtypes = [P, P, U, U, D, P, P]
         _r = L
     return _r
 
@@ -219,6 +225,19 @@ def ref_solve(s, method: str, F, u0=None, phi=None, tol=0.0, restart=0, max_iter
     if rc != 0:
         raise RuntimeError(L.ref_last_error().decode())
     return U, int(it.value), float(sec.value)
+
+
+def toeplitz_case(n: int, seed: int, lower: bool = False):
+    """Seeded Toeplitz test operator (first column, first row), decaying off the
+    diagonal, diagonal 4 (well conditioned for the lower-triangular solves)."""
+    rng = np.random.default_rng(seed)
+    col = rng.standard_normal(n) / (1.0 + np.arange(n)) ** 0.7
+    row = rng.standard_normal(n) / (1.0 + np.arange(n)) ** 0.7
+    col[0] = 4.0
+    row[0] = col[0]
+    if lower:
+        row[1:] = 0.0
+    return col, row
 
 
 def relerr(x, y) -> float:

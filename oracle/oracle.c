@@ -152,6 +152,30 @@ int or_forward_solve(const double* col, const double* b, uint64_t n, double* x) 
     return 0;
 }
 
+/* Reference ToeplitzOperator::entry + DenseMatrix::multiply (toeplitz.hpp:44-46,
+ * toeplitz.cpp:14-23): y = dense(T) x, acc over j ascending.  This is the
+ * reference's own oracle for toeplitz_matvec (toeplitz.hpp:11-12). */
+void or_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y) {
+    for (uint64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (uint64_t j = 0; j < n; ++j) acc += (j >= i ? row[j - i] : col[i - j]) * x[j];
+        y[i] = acc;
+    }
+}
+
+/* Reference block_matvec (toeplitz.cpp:150-167) with the dense diagonal product:
+ * y_b = T x_b, then += beta x_{b-1}, then += beta x_{b+1}. */
+void or_block_matvec(const double* col, const double* row, uint64_t n, uint64_t m, double beta, const double* x,
+                     double* y) {
+    for (uint64_t b = 0; b < m; ++b) {
+        or_toeplitz_matvec(col, row, n, x + b * n, y + b * n);
+        if (b > 0)
+            for (uint64_t k = 0; k < n; ++k) y[b * n + k] += beta * x[(b - 1) * n + k];
+        if (b + 1 < m)
+            for (uint64_t k = 0; k < n; ++k) y[b * n + k] += beta * x[(b + 1) * n + k];
+    }
+}
+
 /* Reference solve_scheme4 Direct, schemes.cpp:434-463.  F: f(x_i, n tau). */
 void or_direct_s4(double gamma, uint64_t cells, uint64_t N, double h, double tau,
                   const double* F, const double* u0, double* U) {

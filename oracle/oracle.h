@@ -21,6 +21,9 @@ void or_rhs_s3(double gamma, uint64_t cells, uint64_t N, double tau, const doubl
                const double* u0, const double* phi, int mode, double* R);
 void or_rhs_ode(double gamma, uint64_t N, double tau, const double* F, double u0, double* R);
 int or_forward_solve(const double* col, const double* b, uint64_t n, double* x);
+void or_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y);
+void or_block_matvec(const double* col, const double* row, uint64_t n, uint64_t m, double beta, const double* x,
+                     double* y);
 void or_direct_s4(double gamma, uint64_t cells, uint64_t N, double h, double tau,
                   const double* F, const double* u0, double* U);
 void or_direct_s3(double gamma, uint64_t cells, uint64_t N, double h, double tau,

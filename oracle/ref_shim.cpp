@@ -139,6 +139,32 @@ int ref_forward_solve(const double* col, const double* b, uint64_t n, double* x)
     }
 }
 
+// embed_circulant + toeplitz_matvec (toeplitz.cpp:84-115): the reference's FFT path
+int ref_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y) {
+    try {
+        auto t = ToeplitzOperator::general(std::vector<double>(col, col + n), std::vector<double>(row, row + n));
+        auto v = toeplitz_matvec(embed_circulant(t), std::span<const double>(x, n));
+        std::memcpy(y, v.data(), sizeof(double) * n);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// BlockTridiagonalToeplitzOperator + block_matvec (toeplitz.cpp:117-167)
+int ref_block_matvec(const double* col, const double* row, uint64_t n, uint64_t m, double beta, const double* x,
+                     double* y) {
+    try {
+        auto t = ToeplitzOperator::general(std::vector<double>(col, col + n), std::vector<double>(row, row + n));
+        BlockTridiagonalToeplitzOperator op(m, t, beta);
+        auto v = block_matvec(op, std::span<const double>(x, n * m));
+        std::memcpy(y, v.data(), sizeof(double) * n * m);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int ref_toeplitz_gmres(const double* col, const double* b, uint64_t n, double tol,
                        uint64_t restart, double* x, uint64_t* iterations) {
     try {

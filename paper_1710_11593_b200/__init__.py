@@ -93,7 +93,8 @@ _lib = None
 
 ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exchange", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
-               "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy")
+               "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy",
+               "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec")
 
 
 def lib() -> C.CDLL:
@@ -107,6 +108,9 @@ def lib() -> C.CDLL:
         L.ft_setup.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(P)]
         L.ft_setup_batch.argtypes = [C.POINTER(_Problem), U64, C.POINTER(_Options), C.POINTER(P)]
         L.ft_setup_partitioned.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), I, I, C.POINTER(P)]
+        L.ft_setup_toeplitz.argtypes = [P, U64, U64, C.POINTER(_Options), C.POINTER(P)]
+        L.ft_toeplitz_matvec.argtypes = [P, P, U64, U64, P, P]
+        L.ft_block_matvec.argtypes = [P, P, U64, U64, C.c_double, P, P]
         L.ft_set_exchange.argtypes = [P, EXCHANGE_FN, P, P, P]
         L.ft_plan_get_info.argtypes = [P, C.POINTER(_Info)]
         L.ft_column.argtypes = [P, U64, P]
@@ -209,21 +213,26 @@ class SchemeSolution:
 
 
 class Plan:
-    """A device-resident solver plan (ft_setup / ft_setup_batch)."""
+    """A device-resident solver plan (ft_setup / ft_setup_batch; Plan.toeplitz for
+    ft_setup_toeplitz)."""
 
     def __init__(self, problems, rhs_mode: int = FT_RHS_REFERENCE, near_field: int = 0,
-                 device: int = -1, partition=None):
-        if isinstance(problems, ProblemSpec):
-            problems = [problems]
-        self.specs = list(problems)
-        arr = (_Problem * len(self.specs))(*[p._c() for p in self.specs])
-        opt = _Options(rhs_mode, near_field, device, 0)
-        h = C.c_void_p()
-        if partition is None:
-            _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))
+                 device: int = -1, partition=None, _handle=None):
+        if _handle is not None:
+            self.specs = []
+            h = _handle
         else:
-            rank, world = partition
-            _check(lib().ft_setup_partitioned(arr, C.byref(opt), rank, world, C.byref(h)))
+            if isinstance(problems, ProblemSpec):
+                problems = [problems]
+            self.specs = list(problems)
+            arr = (_Problem * len(self.specs))(*[p._c() for p in self.specs])
+            opt = _Options(rhs_mode, near_field, device, 0)
+            h = C.c_void_p()
+            if partition is None:
+                _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))
+            else:
+                rank, world = partition
+                _check(lib().ft_setup_partitioned(arr, C.byref(opt), rank, world, C.byref(h)))
         self._h = h
         info = _Info()
         _check(lib().ft_plan_get_info(self._h, C.byref(info)))
@@ -233,6 +242,17 @@ class Plan:
         self.global_nodes = int(info.nodes)
         self.node_begin = int(info.node_begin)
         self.N = int(info.time_steps)
+
+    @classmethod
+    def toeplitz(cls, first_cols, device: int = -1) -> "Plan":
+        """Lower-triangular Toeplitz systems with the caller's first columns
+        ([count][n] or [n]); ToeplitzOperator::lower_triangular +
+        lower_toeplitz_forward_solve (toeplitz.cpp:169-186).  Buffers are [count][n]."""
+        cols = np.atleast_2d(np.ascontiguousarray(first_cols, dtype=np.float64))
+        opt = _Options(0, 0, device, 0)
+        h = C.c_void_p()
+        _check(lib().ft_setup_toeplitz(cols.ctypes.data, cols.shape[1], cols.shape[0], C.byref(opt), C.byref(h)))
+        return cls(None, _handle=h)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -317,6 +337,41 @@ def schedule(time_steps: int, leaf: int = 32):
     _check(lib().ft_schedule(time_steps, leaf, arr, cap, C.byref(cnt)))
     return [dict(kind=arr[i].kind, level=arr[i].level, t0=arr[i].t0, len=arr[i].len)
             for i in range(cnt.value)]
+
+
+def toeplitz_matvec(first_col, x, first_row=None):
+    """y = T x for one vector [n] or a batch [count][n] (reference toeplitz_matvec,
+    toeplitz.cpp:98-115; first_row None = lower triangular).  numpy or torch
+    (host or CUDA) arrays; returns the same kind."""
+    col = np.ascontiguousarray(first_col, dtype=np.float64)
+    row = None if first_row is None else np.ascontiguousarray(first_row, dtype=np.float64)
+    n = col.shape[0]
+    count = int(np.prod(x.shape)) // n
+    y = np.empty_like(x) if isinstance(x, np.ndarray) else x.new_empty(x.shape)
+    _check(lib().ft_toeplitz_matvec(col.ctypes.data, None if row is None else row.ctypes.data, n, count,
+                                    _ptr(x), _ptr(y)))
+    return y
+
+
+def block_matvec(first_col, m_blocks: int, off_scale: float, x, first_row=None):
+    """Block tridiagonal Toeplitz operator apply (reference block_matvec,
+    toeplitz.cpp:150-167); x is [m_blocks * n] or [m_blocks][n]."""
+    col = np.ascontiguousarray(first_col, dtype=np.float64)
+    row = None if first_row is None else np.ascontiguousarray(first_row, dtype=np.float64)
+    y = np.empty_like(x) if isinstance(x, np.ndarray) else x.new_empty(x.shape)
+    _check(lib().ft_block_matvec(col.ctypes.data, None if row is None else row.ctypes.data, col.shape[0], m_blocks,
+                                 float(off_scale), _ptr(x), _ptr(y)))
+    return y
+
+
+def lower_toeplitz_solve(first_col, b, method: SolveMethod = SolveMethod.Fast):
+    """x with T x = b, T lower-triangular Toeplitz (reference
+    lower_toeplitz_forward_solve, toeplitz.cpp:169-186) -- the D&C (Fast) or
+    the reference's substitution order (Direct)."""
+    plan = Plan.toeplitz(first_col)
+    bb = np.ascontiguousarray(b, dtype=np.float64).reshape(plan.shape) if isinstance(b, np.ndarray) else b
+    x, _ = (plan.solve_fast if method == SolveMethod.Fast else plan.solve_direct)(bb)
+    return x.reshape(np.shape(b)) if isinstance(b, np.ndarray) else x
 
 
 def solve(spec: ProblemSpec, method: SolveMethod = SolveMethod.Fast, rhs_mode: int = 0) -> SchemeSolution:

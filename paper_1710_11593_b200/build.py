@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str
           "-I", str(CSRC)]
 # per-file extra flags: the direct path must round exactly like the reference
 EXTRA = {"direct.cu": ["--fmad=false"]}
-SOURCES = ["api.cu", "leaf.cu", "mp.cu", "direct.cu"]
+SOURCES = ["api.cu", "leaf.cu", "mp.cu", "direct.cu", "toeplitz.cu"]
 
 
 def nvcc() -> str:

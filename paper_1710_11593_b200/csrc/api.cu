@@ -61,6 +61,7 @@ struct ft_plan {
     int nodes = 1;
     double h = 0, tau = 0;
     int rhs_mode = 0;
+    bool custom = false;  // ft_setup_toeplitz plan (caller's columns, no RHS assembly)
     int J = 1;
     int device = 0;
     std::vector<double> gamma;
@@ -331,7 +332,7 @@ int ensure_work(ft_plan* p) {
 }
 
 int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, ft_plan** out, int rank = 0,
-               int world = 1) {
+               int world = 1, const double* custom_cols = nullptr) {
     if (!probs || !out || count == 0) return set_err(FT_EINVAL, "ft_setup: null argument");
     *out = nullptr;
     for (uint64_t b = 0; b < count; ++b) {
@@ -428,6 +429,17 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
                 pc.off = 0.0;
                 for (uint64_t j = 0; j < N; ++j) dw[b * N + j] = col[j];
             }
+        }
+    }
+
+    if (custom_cols) {  // ft_setup_toeplitz: caller's lower-triangular columns, no scheme
+        p->custom = true;
+        for (uint64_t b = 0; b < count; ++b) {
+            double* col = p->col_h.data() + b * N;
+            std::memcpy(col, custom_cols + b * N, sizeof(double) * N);
+            p->pc_h[b].d = col[0];
+            p->pc_h[b].off = 0.0;
+            for (uint64_t j = 0; j < N; ++j) dw[b * N + j] = col[j];
         }
     }
 
@@ -693,6 +705,100 @@ extern "C" {
 
 const char* ft_last_error(void) { return g_err.c_str(); }
 
+int ft_setup_toeplitz(const double* first_cols, uint64_t n, uint64_t count, const ft_options* options,
+                      ft_plan** out) {
+    if (!first_cols || !out || n == 0 || count == 0) return set_err(FT_EINVAL, "ft_setup_toeplitz: bad argument");
+    if (is_device_ptr(first_cols)) return set_err(FT_EINVAL, "ft_setup_toeplitz: host columns expected");
+    for (uint64_t b = 0; b < count; ++b)  // toeplitz.cpp:175-176
+        if (first_cols[b * n] == 0.0) return set_err(FT_ESOLVER, "lower_toeplitz_forward_solve: zero diagonal");
+    std::vector<ft_problem> probs(count, ft_problem{FT_SCHEME_ODE, 0.5, n, 0, 1.0, 1.0});
+    return setup_impl(probs.data(), count, options, out, 0, 1, first_cols);
+}
+
+// y = T x (or the block operator) for count vectors; col/row/x/y host or device
+static int toeplitz_apply(const double* col, const double* row, uint64_t n, uint64_t count, const double* x,
+                          double* y, double beta, int block_mode) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(FT_ECUDA, "no CUDA device available (this library has no CPU path)");
+    }
+    const cudaStream_t st = cudaStreamPerThread;
+    const size_t vb = sizeof(double) * n * count, cb = sizeof(double) * n;
+    double *dcol = nullptr, *drow = nullptr, *dx = nullptr, *dy = nullptr;
+    auto cleanup = [&]() {
+        if (dcol) cudaFree(dcol);
+        if (drow) cudaFree(drow);
+        if (dx && dx != x) cudaFree(dx);
+        if (dy && dy != y) cudaFree(dy);
+    };
+    std::vector<double> lrow;
+    if (!row) {  // ToeplitzOperator::lower_triangular (toeplitz.cpp:42-47)
+        double c0 = 0.0;
+        if (is_device_ptr(col)) {
+            if (cudaMemcpy(&c0, col, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return set_err(FT_ECUDA, "copy");
+        } else {
+            c0 = col[0];
+        }
+        lrow.assign(n, 0.0);
+        lrow[0] = c0;
+        row = lrow.data();
+    }
+    if (cudaMalloc(&dcol, cb) != cudaSuccess || cudaMalloc(&drow, cb) != cudaSuccess) {
+        cleanup();
+        return set_err(FT_ENOMEM, "toeplitz matvec: device allocation failed");
+    }
+    cudaMemcpyAsync(dcol, col, cb, cudaMemcpyDefault, st);
+    cudaMemcpyAsync(drow, row, cb, cudaMemcpyDefault, st);
+    double c0 = 0.0, r0 = 0.0;
+    cudaMemcpyAsync(&c0, dcol, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&r0, drow, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (c0 != r0) {  // toeplitz.cpp:31-32
+        cleanup();
+        return set_err(FT_EINVAL, "ToeplitzOperator: first_col[0] must equal first_row[0]");
+    }
+    const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
+    dx = const_cast<double*>(x);
+    dy = y;
+    if (!xdev || x == y) {  // in place needs a copy of x (block mode reads neighbours)
+        if (cudaMalloc(&dx, vb) != cudaSuccess) {
+            dx = nullptr;
+            cleanup();
+            return set_err(FT_ENOMEM, "toeplitz matvec: device allocation failed");
+        }
+        cudaMemcpyAsync(dx, x, vb, cudaMemcpyDefault, st);
+    }
+    if (!ydev) {
+        if (cudaMalloc(&dy, vb) != cudaSuccess) {
+            dy = nullptr;
+            cleanup();
+            return set_err(FT_ENOMEM, "toeplitz matvec: device allocation failed");
+        }
+    }
+    cudaError_t e = launch_toeplitz_matvec(dcol, drow, n, dx, dy, beta, block_mode, count, st);
+    if (e == cudaSuccess && !ydev) e = cudaMemcpyAsync(y, dy, vb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) return set_err(FT_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e));
+    return FT_OK;
+}
+
+int ft_toeplitz_matvec(const double* first_col, const double* first_row, uint64_t n, uint64_t count,
+                       const double* x, double* y) {
+    if (!first_col || !x || !y || count == 0) return set_err(FT_EINVAL, "ft_toeplitz_matvec: null argument");
+    if (n == 0) return set_err(FT_EINVAL, "ToeplitzOperator: empty first column");
+    return toeplitz_apply(first_col, first_row, n, count, x, y, 0.0, 0);
+}
+
+int ft_block_matvec(const double* first_col, const double* first_row, uint64_t n, uint64_t m_blocks,
+                    double off_scale, const double* x, double* y) {
+    if (!first_col || !x || !y) return set_err(FT_EINVAL, "ft_block_matvec: null argument");
+    if (n == 0) return set_err(FT_EINVAL, "ToeplitzOperator: empty first column");
+    if (m_blocks == 0) return set_err(FT_EINVAL, "BlockTridiagonalToeplitzOperator: need at least one block");
+    return toeplitz_apply(first_col, first_row, n, m_blocks, x, y, off_scale, 1);
+}
+
 int ft_setup(const ft_problem* problem, const ft_options* options, ft_plan** out) {
     return setup_impl(problem, 1, options, out);
 }
@@ -756,6 +862,7 @@ int ft_set_stream(ft_plan* p, void* s) {
 // assemble_scheme4 rhs (schemes.cpp:401-408) / Scheme3Rhs (:300-306) / ODE
 int ft_assemble_rhs(const ft_plan* p, ft_forcing_fn f, ft_initial_fn u0, ft_initial_fn phi,
                     void* user, double* rhs) {
+    if (p && p->custom) return set_err(FT_EINVAL, "ft_assemble_rhs: plan from ft_setup_toeplitz has no scheme");
     if (!p || !rhs) return set_err(FT_EINVAL, "ft_assemble_rhs: null argument");
     if (!f) return set_err(FT_EINVAL, "ProblemSpec: forcing callback is required");
     const uint64_t N = p->N;
@@ -785,6 +892,7 @@ int ft_assemble_rhs(const ft_plan* p, ft_forcing_fn f, ft_initial_fn u0, ft_init
 
 int ft_assemble_rhs_grid(const ft_plan* p, const double* F, const double* u0, const double* phi,
                          double* rhs) {
+    if (p && p->custom) return set_err(FT_EINVAL, "ft_assemble_rhs: plan from ft_setup_toeplitz has no scheme");
     if (!p || !F || !rhs) return set_err(FT_EINVAL, "ft_assemble_rhs_grid: null argument");
     if (is_device_ptr(F) || is_device_ptr(rhs))
         return set_err(FT_EINVAL, "ft_assemble_rhs_grid: host arrays expected");
@@ -816,6 +924,7 @@ int ft_assemble_rhs_grid(const ft_plan* p, const double* F, const double* u0, co
 int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const double* k,
                           const double* pe, const int* trig, const double* u0amp,
                           const double* phiamp, double* rhs) {
+    if (p && p->custom) return set_err(FT_EINVAL, "ft_assemble_rhs: plan from ft_setup_toeplitz has no scheme");
     if (!p || !rhs || nmodes < 0 || (nmodes && (!a || !k || !pe || !trig)))
         return set_err(FT_EINVAL, "ft_assemble_rhs_modes: bad argument");
     if (!is_device_ptr(rhs)) return set_err(FT_EINVAL, "ft_assemble_rhs_modes: rhs must be device memory");

@@ -147,5 +147,7 @@ cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int c
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
+cudaError_t launch_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y,
+                                   double beta, int block_mode, uint64_t vectors, cudaStream_t st);
 
 }  // namespace ftb

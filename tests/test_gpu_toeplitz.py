@@ -1,0 +1,80 @@
+"""GPU: the reference's structured-operator API (toeplitz.hpp) through the C ABI.
+
+* ft_toeplitz_matvec / ft_block_matvec against the oracle's dense product (the
+  reference's own oracle form, toeplitz.cpp:14-23) -- tight, the GPU sums
+  directly -- and therefore within FFT rounding of the reference's
+  toeplitz_matvec (pinned on CPU in test_oracle.py);
+* ft_setup_toeplitz: the D&C (fast) and the reference's substitution order
+  (direct, bitwise) for lower_toeplitz_forward_solve (toeplitz.cpp:169-186);
+* the reference's error behaviour (zero diagonal, col0 != row0).
+"""
+import numpy as np
+import pytest
+
+
+
+def _dense_or(oracle_mod, col, row, x):
+    y = np.empty_like(x)
+    oracle_mod.olib().or_toeplitz_matvec(col.ctypes.data, row.ctypes.data, col.shape[0], x.ctypes.data, y.ctypes.data)
+    return y
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,count,lower", [(1, 1, False), (5, 3, False), (1000, 2, True), (4097, 1, False),
+                                           (65536, 1, True)])
+def test_toeplitz_matvec(ft, oracle_mod, n, count, lower):
+    import torch
+
+    col, row = oracle_mod.toeplitz_case(n, n, lower)
+    X = np.random.default_rng(n).standard_normal((count, n))
+    Y = ft.toeplitz_matvec(col, X, None if lower else row)
+    ref = np.stack([_dense_or(oracle_mod, col, row, X[b]) for b in range(count)])
+    scale = np.abs(col).sum() + np.abs(row).sum()
+    assert np.max(np.abs(Y - ref)) <= 1e-14 * scale * np.max(np.abs(X))
+    Xd = torch.from_numpy(X).cuda()
+    Yd = ft.toeplitz_matvec(col, Xd, None if lower else row)  # device buffers
+    assert np.array_equal(Yd.cpu().numpy(), Y)
+
+
+@pytest.mark.gpu
+def test_block_matvec(ft, oracle_mod):
+    n, m, beta = 3000, 7, 0.41
+    col, row = oracle_mod.toeplitz_case(n, 11)
+    x = np.random.default_rng(4).standard_normal(n * m)
+    y = ft.block_matvec(col, m, beta, x, row)
+    ref = np.empty_like(x)
+    oracle_mod.olib().or_block_matvec(col.ctypes.data, row.ctypes.data, n, m, beta, x.ctypes.data, ref.ctypes.data)
+    scale = np.abs(col).sum() + np.abs(row).sum() + 2 * abs(beta)
+    assert np.max(np.abs(y - ref)) <= 1e-14 * scale * np.max(np.abs(x))
+    xi = x.copy()
+    ft.lib().ft_block_matvec(col.ctypes.data, row.ctypes.data, n, m, beta, xi.ctypes.data, xi.ctypes.data)
+    assert np.array_equal(xi, y)  # in place
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,count", [(1, 1), (33, 2), (4096, 1), (20000, 3)])
+def test_lower_toeplitz_solve(ft, oracle_mod, n, count):
+    rng = np.random.default_rng(n)
+    cols = np.stack([oracle_mod.toeplitz_case(n, n + b, True)[0] for b in range(count)])
+    B = rng.standard_normal((count, n))
+    plan = ft.Plan.toeplitz(cols)
+    Xf, _ = plan.solve_fast(B)
+    Xd, _ = plan.solve_direct(B)
+    for b in range(count):
+        xo = np.empty(n)
+        assert oracle_mod.olib().or_forward_solve(cols[b].ctypes.data, B[b].ctypes.data, n, xo.ctypes.data) == 0
+        assert np.array_equal(Xd[b], xo)  # reference summation order, bitwise
+        assert oracle_mod.relerr(Xf[b], xo) <= 1e-10
+    x1 = ft.lower_toeplitz_solve(cols[0], B[0])
+    assert x1.shape == (n,) and np.array_equal(x1, Xf[0])
+
+
+@pytest.mark.gpu
+def test_toeplitz_errors(ft):
+    with pytest.raises(ft.FractimeError, match="lower_toeplitz_forward_solve: zero diagonal"):
+        ft.Plan.toeplitz(np.array([0.0, 1.0, 2.0]))
+    with pytest.raises(ft.InvalidArgument, match="first_col\\[0\\] must equal first_row\\[0\\]"):
+        ft.toeplitz_matvec(np.array([1.0, 2.0]), np.ones(2), np.array([3.0, 4.0]))
+    plan = ft.Plan.toeplitz(np.array([2.0, 1.0]))
+    with pytest.raises(ft.InvalidArgument, match="no scheme"):
+        plan.assemble_rhs_grid(np.zeros((1, 2)))

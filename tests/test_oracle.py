@@ -134,3 +134,33 @@ def test_scheme3_rhs_modes(oracle_mod):
     s = w.specs[0]
     oracle_mod.olib().or_constants(2, s.gamma, s.tau(), mu.ctypes.data, c.ctypes.data)
     assert np.allclose(R1[:, 0] - R0[:, 0], c[0] * u0, rtol=1e-12)
+
+
+@pytest.mark.parametrize("n,lower", [(1, False), (7, False), (64, True), (300, False), (1025, True)])
+def test_toeplitz_matvec_oracle_vs_reference(oracle_mod, n, lower):
+    """or_toeplitz_matvec (dense, the reference's own oracle form) against the
+    reference's FFT path (embed_circulant + toeplitz_matvec, toeplitz.cpp:84-115)."""
+    r = oracle_mod.rlib()
+    if r is None:
+        pytest.skip("oracle/_ref not built")
+    col, row = oracle_mod.toeplitz_case(n, n, lower)
+    x = np.random.default_rng(1).standard_normal(n)
+    y_or, y_ref = np.empty(n), np.empty(n)
+    oracle_mod.olib().or_toeplitz_matvec(col.ctypes.data, row.ctypes.data, n, x.ctypes.data, y_or.ctypes.data)
+    assert r.ref_toeplitz_matvec(col.ctypes.data, row.ctypes.data, n, x.ctypes.data, y_ref.ctypes.data) == 0
+    dense = np.array([[row[j - i] if j >= i else col[i - j] for j in range(n)] for i in range(n)])
+    assert np.allclose(y_or, dense @ x, rtol=0, atol=1e-13 * np.abs(dense).sum(1).max() * np.abs(x).max())
+    assert np.max(np.abs(y_or - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+
+
+def test_block_matvec_oracle_vs_reference(oracle_mod):
+    r = oracle_mod.rlib()
+    if r is None:
+        pytest.skip("oracle/_ref not built")
+    n, m, beta = 200, 5, -0.37
+    col, row = oracle_mod.toeplitz_case(n, 3)
+    x = np.random.default_rng(2).standard_normal(n * m)
+    y_or, y_ref = np.empty(n * m), np.empty(n * m)
+    oracle_mod.olib().or_block_matvec(col.ctypes.data, row.ctypes.data, n, m, beta, x.ctypes.data, y_or.ctypes.data)
+    assert r.ref_block_matvec(col.ctypes.data, row.ctypes.data, n, m, beta, x.ctypes.data, y_ref.ctypes.data) == 0
+    assert np.max(np.abs(y_or - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
