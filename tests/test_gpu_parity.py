@@ -243,3 +243,23 @@ def test_streamed_host_solve(ft, oracle_mod, cid, kw):
     if w.N * w.nodes * w.B <= 3_000_000:
         F, u0, phi = _inputs(oracle_mod, w)
         assert oracle_mod.relerr(hU.numpy(), oracle_mod.direct(w, F, u0, phi)) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference")])
+def test_harness_convergence_tables(ft, eid, key):
+    """The GPU harness (device RHS, fast D&C) reproduces the reference's frozen
+    convergence tables (acceptance.cpp:206-255) in the reference CSV format."""
+    import json
+    from pathlib import Path
+
+    from paper_1710_11593_b200 import harness as H
+
+    col = json.loads((Path(__file__).resolve().parent / "golden" / "tables.json").read_text())[key][1]
+    rows = H.run_convergence(eid, [col["gamma"]], H.exponent_ladder(3, 8))
+    for r, err in zip(rows, col["errors"]):
+        assert abs(r.l2_error - err) <= 0.05 * err
+    for r, rate in zip(rows[1:], col["rates"]):
+        assert abs(r.rate - rate) <= 0.05
+    csv = H.emit_csv(rows).splitlines()
+    assert len(csv) == 7 and all(len(line.split(",")) == 10 for line in csv)

@@ -109,3 +109,17 @@ def test_workload_shapes():
     assert w3.specs[0].tau() == 1.0 / 65536  # time-prefix keeps tau exact
     w3n = W.config(3, cells=17)
     assert w3n.specs[0].h() == 1.0 / 1025  # node-prefix keeps h exact
+
+
+def test_harness_csv_format():
+    """emit_csv restates the reference harness's CSV (harness.cpp:296-304)."""
+    from paper_1710_11593_b200 import harness as H
+
+    rows = [H.ConvergenceRow(3, 0.125, 0.125, 0.0084669, None, 0, 0.25, "fast", 0.1, "diffusion"),
+            H.ConvergenceRow(4, 0.0625, 0.0625, 0.0021203, 1.9975, 0, 0.5, "fast", 0.1, "diffusion")]
+    lines = H.emit_csv(rows).splitlines()
+    assert lines[0] == "mesh_exp,h,tau,l2_error,rate,iterations,wall_seconds,method,gamma,scheme"
+    assert lines[1] == "3,0.125,0.125,%.17g,,0,0.25,fast,0.10000000000000001,diffusion" % 0.0084669
+    assert lines[2].split(",")[4] == "%.17g" % 1.9975
+    assert H.exponent_ladder(3, 5) == [(3, 8, 8), (4, 16, 16), (5, 32, 32)]
+    assert H.exponent_ladder(2, 3, 10) == [(2, 1024, 4), (3, 1024, 8)]
