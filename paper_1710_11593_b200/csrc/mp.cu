@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fft.cuh"
 #include "internal.cuh"
@@ -523,6 +524,157 @@ __global__ void __launch_bounds__(kMpThreads, FT_MP1_MINB) mp1_kernel(MpArgs a) 
     }
 }
 
+// ---- group-private variant (n <= kMpTile): no CTA-wide barriers -------------
+// Every pass of the n-point transform of pair g touches only that pair's SMEM
+// region, and with the task numbering below the n/16 threads that own it form a
+// contiguous group (half a warp for n = 256, a warp for 512, 2/4 warps for
+// 1024/2048).  Groups synchronise privately (__syncwarp or a named barrier per
+// group), so they drift out of phase: one group's HBM loads overlap another's
+// FFT work instead of the whole CTA waiting at each barrier.
+template <int LOGN>
+struct GroupSync {
+    static constexpr int GT = (1 << LOGN) / 16;  // threads per pair
+    __device__ static __forceinline__ void sync(int g) {
+        if constexpr (GT <= 32) {
+            __syncwarp();
+        } else if constexpr (GT < kMpThreads) {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GT) : "memory");
+        } else {
+            __syncthreads();
+        }
+    }
+};
+
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_fwd_g(cplx* buf, int total, const cplx* tw, int g) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        GroupSync<LOGN>::sync(g);
+        pass_c<16, LOGS, false>(buf, total, tw);
+        mid_fwd_g<LOGS - 4, LOGN>(buf, total, tw, g);
+    }
+}
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_inv_g(cplx* buf, int total, const cplx* tw, int g) {
+    if constexpr (LOGS > lg2c(Plan1<LOGN>::RL)) {
+        mid_inv_g<LOGS - 4, LOGN>(buf, total, tw, g);
+        GroupSync<LOGN>::sync(g);
+        pass_c<16, LOGS, true>(buf, total, tw);
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
+    using PL = Plan1<LOGN>;
+    constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
+    static_assert(n <= kMpTile, "group-private plan needs n <= kMpTile");
+    constexpr int G = kMpTile / n, GT = n / 16;
+    constexpr int total = kMpTile;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int g = tid / GT, j = tid - g * GT;  // pass-0 / last-pass task tid: pair g, column j (GT == Q0)
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const int pair = blockIdx.x * G + g;
+    const bool live = pair < npairs;
+    const uint64_t N = a.N;
+    PairInfo pi;
+    {
+        const int rp = min(pair, npairs - 1);
+        const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+        pi = {(uint64_t)(pb * a.nodes + 2 * lp), pb, (live && 2 * lp + 1 < a.nodes) ? 1 : 0};
+    }
+
+    // pass 0 (S = n, radix 16) from HBM; inputs p >= 8 are the zero padding
+    {
+        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        cplx v[16];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            v[p].x = live ? x1[(uint64_t)p * Q0] : 0.0;
+            v[p].y = (live && pi.has2) ? x1[N + (uint64_t)p * Q0] : 0.0;
+        }
+        dft_reg_halfzero<16>(v);
+        cplx w[16];
+        pass_twiddles<16>(w, a.tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], w[q]);
+        const int pb = sphys(g * n + j);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) buf[pb + q * (Q0 + (Q0 >> 4))] = v[q];
+    }
+    mid_fwd_g<LOGN - 4, LOGN>(buf, total, a.tw, g);
+
+    // fused pass: this group's tasks t = g*(n/RL) + j + k*GT, k < 16/RL
+    constexpr int FT = 16 / RL;
+    cplx spv[16];
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+        const int base = (g * (n / RL) + j + k * GT) * RL;
+        const cplx* sp = a.spec + (uint64_t)pi.pb * n + (base & (n - 1));
+#pragma unroll
+        for (int p = 0; p < RL; ++p) spv[k * RL + p] = ldgc(&sp[p]);
+    }
+    GroupSync<LOGN>::sync(g);
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+        const int pbx = sphys((g * (n / RL) + j + k * GT) * RL);
+        cplx v[RL];
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+        dft_reg<RL, false>(v);
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], spv[k * RL + p]);
+        dft_reg<RL, true>(v);
+#pragma unroll
+        for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+    }
+    mid_inv_g<LOGN - 4, LOGN>(buf, total, a.tw, g);
+
+    // last inverse pass (S = n, radix 16): outputs p >= 8 are the targets [mid, mid + h)
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    double r1[8], r2[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
+        const bool ok = live && tt < tend;
+        r1[p] = ok ? a.rsrc[pi.row1 * N + tt] : 0.0;
+        r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
+    }
+    cplx w[16];
+    pass_twiddles<16>(w, a.tw, n, j);
+    GroupSync<LOGN>::sync(g);
+    const int pbx = sphys(g * n + j);
+    cplx v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = buf[pbx + q * (Q0 + (Q0 >> 4))];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) v[q] = cmulc(v[q], w[q]);
+    dft_reg<16, true>(v);
+    if (!live) return;
+#pragma unroll
+    for (int p = 8; p < 16; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)(p - 8) * Q0;
+        if (tt >= tend) continue;
+        cplx y = v[p];
+        const int tp = (int)(tt - a.mid);
+        if (tp < a.J - 1) {  // exact near field: lags t - j < J
+            const double* cp = a.col + (uint64_t)pi.pb * N;
+            const double* xr = a.X + pi.row1 * N;
+            const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
+            double s1 = 0.0, s2 = 0.0;
+            for (uint64_t jj = a.mid; jj-- > jlo;) {
+                const double cv = cp[tt - jj];
+                s1 = fma(cv, xr[jj], s1);
+                if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
+            }
+            y.x += s1;
+            y.y += s2;
+        }
+        a.X[pi.row1 * N + tt] = r1[p - 8] - y.x;
+        if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 8] - y.y;
+    }
+}
+
 // Spectrum of one level for the single-CTA plan: full n-point column (lags
 // J <= k < min(n, N)), same passes, scaled 1/n, stored in plan order.
 template <int LOGN>
@@ -788,6 +940,18 @@ static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
     }
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
     const int ctas = (npairs + G - 1) / G;
+    if constexpr (n <= kMpTile) {
+        static const bool cta_sync = getenv("FT_MP1_CTA") != nullptr;  // A/B switch
+        if (!cta_sync) {
+            static bool gattr = false;
+            if (!gattr) {
+                cudaFuncSetAttribute(mp1g_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                gattr = true;
+            }
+            mp1g_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
     mp1_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
