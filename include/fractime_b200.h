@@ -13,11 +13,15 @@
  *                                 assemble_scheme3_reordered()      src/schemes.cpp:272-288
  *                                 embed_circulant() (spectra)       src/toeplitz.cpp:84-96
  *   ft_column                  <- ToeplitzOperator::first_col()     include/fractime/toeplitz.hpp:38
+ *                                 assemble_scheme2_reordered()      src/schemes.cpp:149-167
  *   ft_assemble_rhs            <- assemble_scheme4() rhs            src/schemes.cpp:401-408
  *                                 Scheme3Rhs::operator()            src/schemes.cpp:300-306
- *   ft_solve_direct            <- solve(spec, SolveMethod::Direct)  src/schemes.cpp:434-463, :333-352
+ *                                 Scheme2Rhs::operator()            src/schemes.cpp:183-187
+ *   ft_solve_direct            <- solve(spec, SolveMethod::Direct)  src/schemes.cpp:434-463, :333-352,
+ *                                                                    :210-232
  *                                 lower_toeplitz_forward_solve()    src/toeplitz.cpp:169-186
- *   ft_solve_fast              <- solve(spec, SolveMethod::Fast)    src/schemes.cpp:464-474, :353-369
+ *   ft_solve_fast              <- solve(spec, SolveMethod::Fast)    src/schemes.cpp:464-474, :353-369,
+ *                                                                    :233-257
  *                                 (GMRES + FFT matvec, src/krylov.cpp:107-223, replaced by a
  *                                 time-axis divide-and-conquer; same system, same answer)
  *   ft_setup_toeplitz          <- ToeplitzOperator::lower_triangular() include/fractime/toeplitz.hpp:33
@@ -59,10 +63,12 @@ extern "C" {
 
 /* Scheme ids follow the reference enum SchemeId (schemes.hpp:182):
  * Ode2Sided=0 (here: the one-sided fractional ODE of BASELINE config 1, built
- * from the reference Toeplitz API as in SURVEY.md 3.4), Hyperbolic=1 (not
- * provided), DiffusionWave=2 (reference Scheme 3), Diffusion=3 (Scheme 4). */
+ * from the reference Toeplitz API as in SURVEY.md 3.4), Hyperbolic=1
+ * (reference Scheme 2, transport; at most 2048 interior nodes per problem),
+ * DiffusionWave=2 (reference Scheme 3), Diffusion=3 (Scheme 4). */
 enum {
     FT_SCHEME_ODE = 0,
+    FT_SCHEME_HYPERBOLIC = 1,
     FT_SCHEME_WAVE = 2,
     FT_SCHEME_DIFFUSION = 3
 };
@@ -126,7 +132,8 @@ typedef struct ft_plan_info {
 typedef struct ft_plan ft_plan;
 
 /* forcing(x, t, user) and initial data u0(x, user) / phi(x, user), evaluated
- * at the reference's points: diffusion/ODE (i h, n tau); wave (i h, (n-1/2) tau). */
+ * at the reference's points: diffusion/ODE (i h, n tau); wave (i h, (n-1/2) tau);
+ * hyperbolic forcing ((i-1/2) h, n tau) and u0 at x_i and x_(i-1). */
 typedef double (*ft_forcing_fn)(double x, double t, void* user);
 typedef double (*ft_initial_fn)(double x, void* user);
 
@@ -153,7 +160,8 @@ int ft_column(const ft_plan* plan, uint64_t problem, double* col_host);
 int ft_assemble_rhs(const ft_plan* plan, ft_forcing_fn forcing, ft_initial_fn u0,
                     ft_initial_fn phi, void* user, double* rhs_host);
 /* Same, from the forcing already sampled at the scheme's points (node-major
- * grid F) and initial data arrays (nodes per problem, NULL = 0). */
+ * grid F) and initial data arrays (nodes per problem, NULL = 0; the hyperbolic
+ * scheme's u0 holds nodes + 1 values per problem, x_0 .. x_{cells-1}). */
 int ft_assemble_rhs_grid(const ft_plan* plan, const double* forcing_grid, const double* u0,
                          const double* phi, double* rhs);
 /* Device generation of a separable forcing

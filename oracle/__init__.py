@@ -20,7 +20,7 @@ HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libfractime_ref.so"
 
-OR_ODE, OR_WAVE, OR_DIFFUSION = 0, 2, 3
+OR_ODE, OR_HYPER, OR_WAVE, OR_DIFFUSION = 0, 1, 2, 3
 
 _o = None
 _r = None
@@ -48,6 +48,9 @@ def olib():
         L.or_weights.argtypes = [D, U, P]
         L.or_col_s4.argtypes = [D, U, D, D, P]
         L.or_col_s3.argtypes = [D, U, D, D, P]
+        L.or_col_s2.argtypes = [D, U, D, D, P, P]
+        L.or_rhs_s2.argtypes = [D, U, U, D, P, P, P]
+        L.or_direct_s2.argtypes = [D, U, U, D, D, P, P, P]
         L.or_col_ode.argtypes = [D, U, D, P]
         L.or_rhs_s4.argtypes = [D, U, U, D, P, P, P]
         L.or_rhs_s3.argtypes = [D, U, U, D, P, P, P, I, P]
@@ -61,7 +64,7 @@ def olib():
         L.or_direct_s4.argtypes = [D, U, U, D, D, P, P, P]
         L.or_direct_s3.argtypes = [D, U, U, D, D, P, P, P, I, P]
         L.or_march_ld.argtypes = [I, U, U, P, D, P, P]
-        L.or_forcing_modes.argtypes = [U, U, D, D, D, I, P, P, P, P, P]
+        L.or_forcing_modes.argtypes = [U, U, D, D, D, D, I, P, P, P, P, P]
         L.or_sine_grid.argtypes = [U, D, D, P]
         L.or_splitmix64.argtypes = [C.POINTER(U)]
         L.or_splitmix64.restype = U
@@ -99,30 +102,42 @@ def rlib():
 
 def forcing_grid(w) -> np.ndarray:
     """Sample a workload's separable forcing at the reference's points with glibc
-    (x_i = i h, t_n = n tau; wave (n - 1/2) tau).  Returns [B*nodes, N]."""
+    (x_i = i h, t_n = n tau; wave (n - 1/2) tau; Scheme 2 x = (i - 1/2) h).
+    Returns [B*nodes, N]."""
     s0 = w.specs[0]
     N, nodes = s0.time_steps, w.nodes
     ode = int(s0.scheme) == OR_ODE
     shift = -0.5 if int(s0.scheme) == OR_WAVE else 0.0
+    xshift = -0.5 if int(s0.scheme) == OR_HYPER else 0.0
     out = np.empty((w.B * nodes, N))
     trig = np.ascontiguousarray(w.trig, dtype=np.int32)
     for b, s in enumerate(w.specs):
         h = 0.0 if ode else s.space_length / s.space_cells
         cells = 2 if ode else s.space_cells
         Fb = np.empty((nodes, N))
-        olib().or_forcing_modes(cells, N, h, s.tau(), shift, len(w.k), _d(w.a[b]), _d(w.k), _d(w.p[b]),
+        olib().or_forcing_modes(cells, N, h, s.tau(), xshift, shift, len(w.k), _d(w.a[b]), _d(w.k), _d(w.p[b]),
                                 trig.ctypes.data, Fb.ctypes.data)
         out[b * nodes:(b + 1) * nodes] = Fb
     return out
 
 
 def initial_grid(w, amp) -> Optional[np.ndarray]:
-    """amp_b * sin(pi x_i) per problem (ODE: amp_b), glibc sin."""
+    """amp_b * sin(pi x_i) per problem (ODE: amp_b), glibc sin.  Scheme 2 takes
+    u0 at x_0 .. x_{cells-1} (its RHS uses u0(x_i) + u0(x_{i-1})): nodes + 1 values
+    per problem, the boundary value first."""
     if amp is None:
         return None
     s0 = w.specs[0]
     if int(s0.scheme) == OR_ODE:
         return np.ascontiguousarray(np.asarray(amp, dtype=np.float64))
+    if int(s0.scheme) == OR_HYPER:
+        out = np.empty(w.B * (w.nodes + 1))
+        for b, s in enumerate(w.specs):
+            seg = np.empty(w.nodes)
+            olib().or_sine_grid(s.space_cells, s.space_length / s.space_cells, float(amp[b]), seg.ctypes.data)
+            out[b * (w.nodes + 1)] = float(amp[b]) * 0.0  # amp * sin(pi * 0)
+            out[b * (w.nodes + 1) + 1:(b + 1) * (w.nodes + 1)] = seg
+        return out
     out = np.empty(w.B * w.nodes)
     for b, s in enumerate(w.specs):
         seg = np.empty(w.nodes)
@@ -141,9 +156,12 @@ def direct(w, F, u0=None, phi=None, rhs_mode: int = 0) -> np.ndarray:
     for b, s in enumerate(w.specs):
         Fb = np.ascontiguousarray(F[b * nodes:(b + 1) * nodes])
         Ub = np.empty((nodes, N))
-        u0b = None if u0 is None else np.ascontiguousarray(u0[b * nodes:(b + 1) * nodes])
+        u0b = None if (u0 is None or int(s.scheme) == OR_HYPER) else np.ascontiguousarray(u0[b * nodes:(b + 1) * nodes])
         phib = None if phi is None else np.ascontiguousarray(phi[b * nodes:(b + 1) * nodes])
-        if int(s.scheme) == OR_DIFFUSION:
+        if int(s.scheme) == OR_HYPER:
+            u0h = None if u0 is None else np.ascontiguousarray(u0[b * (nodes + 1):(b + 1) * (nodes + 1)])
+            olib().or_direct_s2(s.gamma, s.space_cells, N, s.h(), s.tau(), _d(Fb), _d(u0h), Ub.ctypes.data)
+        elif int(s.scheme) == OR_DIFFUSION:
             olib().or_direct_s4(s.gamma, s.space_cells, N, s.h(), s.tau(), _d(Fb), _d(u0b), Ub.ctypes.data)
         elif int(s.scheme) == OR_WAVE:
             olib().or_direct_s3(s.gamma, s.space_cells, N, s.h(), s.tau(), _d(Fb), _d(u0b), _d(phib),
@@ -164,6 +182,8 @@ def column(s) -> np.ndarray:
     col = np.empty(N)
     if int(s.scheme) == OR_DIFFUSION:
         olib().or_col_s4(s.gamma, N, s.h(), s.tau(), col.ctypes.data)
+    elif int(s.scheme) == OR_HYPER:
+        olib().or_col_s2(s.gamma, N, s.h(), s.tau(), col.ctypes.data, None)
     elif int(s.scheme) == OR_WAVE:
         olib().or_col_s3(s.gamma, N, s.h(), s.tau(), col.ctypes.data)
     else:
@@ -176,12 +196,16 @@ def march_ld(s, R: np.ndarray) -> np.ndarray:
     N = s.time_steps
     col = column(s)
     nodes = R.shape[0]
-    kind = {OR_ODE: 0, OR_DIFFUSION: 1, OR_WAVE: 2}[int(s.scheme)]
+    kind = {OR_ODE: 0, OR_DIFFUSION: 1, OR_WAVE: 2, OR_HYPER: 3}[int(s.scheme)]
     off = 0.0
     if kind == 1:
         off = -1.0 / (s.h() * s.h())
     elif kind == 2:
         off = -1.0 / s.h()
+    elif kind == 3:
+        b = np.empty(N)
+        olib().or_col_s2(s.gamma, N, s.h(), s.tau(), col.ctypes.data, b.ctypes.data)
+        off = -float(b[0])
     U = np.empty((nodes, N))
     Rc = np.ascontiguousarray(R, dtype=np.float64)
     olib().or_march_ld(kind, nodes, N, col.ctypes.data, off, Rc.ctypes.data, U.ctypes.data)
@@ -195,7 +219,10 @@ def rhs(w, F, u0=None, phi=None, rhs_mode=0) -> np.ndarray:
     for b, s in enumerate(w.specs):
         Fb = np.ascontiguousarray(F[b * nodes:(b + 1) * nodes])
         Rb = np.empty((nodes, N))
-        if int(s.scheme) == OR_DIFFUSION:
+        if int(s.scheme) == OR_HYPER:
+            u0h = None if u0 is None else np.ascontiguousarray(u0[b * (nodes + 1):(b + 1) * (nodes + 1)])
+            olib().or_rhs_s2(s.gamma, s.space_cells, N, s.tau(), _d(Fb), _d(u0h), Rb.ctypes.data)
+        elif int(s.scheme) == OR_DIFFUSION:
             u0b = None if u0 is None else np.ascontiguousarray(u0[b * nodes:(b + 1) * nodes])
             olib().or_rhs_s4(s.gamma, s.space_cells, N, s.tau(), _d(Fb), _d(u0b), Rb.ctypes.data)
         elif int(s.scheme) == OR_WAVE:

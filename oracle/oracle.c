@@ -45,6 +45,7 @@ void or_constants(int scheme, double gamma, double tau, double* mu, double* c) {
     *mu = pow(tau, -g) / tgamma(2.0 - g);
     switch (scheme) {
         case OR_ODE: *c = *mu; break;
+        case OR_HYPER: *c = pow(tau, -g) / (2.0 * tgamma(2.0 - g)); break;
         case OR_WAVE: *c = pow(tau, -g) / tgamma(3.0 - g); break;
         case OR_DIFFUSION: *c = pow(tau, -g) / tgamma(2.0 - g); break;
         default: *c = *mu;
@@ -61,6 +62,22 @@ void or_col_s4(double gamma, uint64_t N, double h, double tau, double* col) {
     or_weights(1.0 - gamma, N, g);
     col[0] = 2.0 / (h * h) + c * g[0];
     for (uint64_t j = 1; j < N; ++j) col[j] = c * (g[j] - g[j - 1]);
+    free(g);
+}
+
+/* Scheme 2 (reordered, per node): reference assemble_scheme2_reordered,
+ * schemes.cpp:160-165.  a = A~ first column, b = B~ first column. */
+void or_col_s2(double gamma, uint64_t N, double h, double tau, double* a, double* b) {
+    double mu, c;
+    or_constants(OR_HYPER, gamma, tau, &mu, &c);
+    double* g = (double*)malloc(sizeof(double) * N);
+    or_weights(1.0 - gamma, N, g);
+    a[0] = 1.0 / h + c * g[0];
+    if (b) b[0] = 1.0 / h - c * g[0];
+    for (uint64_t j = 1; j < N; ++j) {
+        a[j] = c * (g[j] - g[j - 1]);
+        if (b) b[j] = c * (g[j - 1] - g[j]);
+    }
     free(g);
 }
 
@@ -126,6 +143,24 @@ void or_rhs_s3(double gamma, uint64_t cells, uint64_t N, double tau, const doubl
         }
     }
     free(m);
+}
+
+/* Scheme 2: reference Scheme2Rhs schemes.cpp:183-187,
+ * R = f(x_{i-1/2}, n tau) + c g_{n-1} (u0(x_i) + u0(x_{i-1})).  F holds the
+ * forcing at ((i - 1/2) h, n tau); u0 holds u0 at x_0 .. x_{cells-1} (cells
+ * values, the left boundary included). */
+void or_rhs_s2(double gamma, uint64_t cells, uint64_t N, double tau, const double* F,
+               const double* u0, double* R) {
+    double mu, c;
+    or_constants(OR_HYPER, gamma, tau, &mu, &c);
+    double* g = (double*)malloc(sizeof(double) * N);
+    or_weights(1.0 - gamma, N, g);
+    for (uint64_t i = 1; i < cells; ++i) {
+        const double us = u0 ? (u0[i] + u0[i - 1]) : 0.0;
+        for (uint64_t n = 1; n <= N; ++n)
+            R[(i - 1) * N + (n - 1)] = F[(i - 1) * N + (n - 1)] + c * g[n - 1] * us;
+    }
+    free(g);
 }
 
 /* ODE: R_n = f(n tau) + mu G_{n-1} u0 (the Scheme-4 RHS pattern, schemes.cpp:407). */
@@ -251,6 +286,39 @@ void or_direct_s3(double gamma, uint64_t cells, uint64_t N, double h, double tau
     free(history);
 }
 
+/* Reference solve_scheme2 Direct, schemes.cpp:210-232 (with Scheme2Rhs
+ * :183-187; u0 as in or_rhs_s2).  F: f((i - 1/2) h, n tau). */
+void or_direct_s2(double gamma, uint64_t cells, uint64_t N, double h, double tau,
+                  const double* F, const double* u0, double* U) {
+    double mu, c;
+    or_constants(OR_HYPER, gamma, tau, &mu, &c);
+    double* g = (double*)malloc(sizeof(double) * N);
+    or_weights(1.0 - gamma, N, g);
+    double* R = (double*)malloc(sizeof(double) * (cells - 1) * N);
+    or_rhs_s2(gamma, cells, N, tau, F, u0, R);
+    double* history = (double*)malloc(sizeof(double) * (cells - 1));
+    memset(U, 0, sizeof(double) * (cells - 1) * N);
+    for (uint64_t n = 1; n <= N; ++n) {
+        for (uint64_t i = 0; i + 1 < cells; ++i) history[i] = 0.0;
+        for (uint64_t k = 1; k < n; ++k) {
+            const double w = c * (g[n - k - 1] - g[n - k]);
+            for (uint64_t i = 1; i < cells; ++i) history[i - 1] += w * U[(i - 1) * N + (k - 1)];
+        }
+        double u_left = 0.0, hist_left = 0.0;
+        for (uint64_t i = 1; i < cells; ++i) {
+            const double value = (R[(i - 1) * N + (n - 1)] + history[i - 1] + hist_left -
+                                  (c * g[0] - 1.0 / h) * u_left) /
+                                 (c * g[0] + 1.0 / h);
+            U[(i - 1) * N + (n - 1)] = value;
+            u_left = value;
+            hist_left = history[i - 1];
+        }
+    }
+    free(g);
+    free(R);
+    free(history);
+}
+
 /* ---- long-double restatements (same recurrences, 64-bit mantissa) -------- */
 
 /* Generic: node-coupled BLTT time march in long double for a given fp64
@@ -258,6 +326,8 @@ void or_direct_s3(double gamma, uint64_t cells, uint64_t N, double h, double tau
  *   kind 0: diagonal     col0 * x = r                      (ODE, cells-1 == 1)
  *   kind 1: tridiagonal  col0 x_i + off (x_{i-1}+x_{i+1})   (Scheme 4)
  *   kind 2: upwind       col0 x_i + off x_{i-1}             (Scheme 3, off=-1/h)
+ *   kind 3: Scheme 2     col0 x_i + off x_{i-1}, off = -B~_0, history on x_i + x_{i-1}
+ *                        (B~_j = -A~_j for j >= 1, schemes.cpp:162-165)
  * The history is summed in long double over all previous steps.  This is the
  * "exact" reference used for the corrected-mode Scheme 3 and to show the
  * reference's own fp64 rounding. */
@@ -270,7 +340,8 @@ void or_march_ld(int kind, uint64_t nodes, uint64_t N, const double* col, double
     for (uint64_t n = 0; n < N; ++n) {
         for (uint64_t i = 0; i < nodes; ++i) {
             long double acc = R[i * N + n];
-            for (uint64_t k = 0; k < n; ++k) acc -= (long double)col[n - k] * X[i * N + k];
+            for (uint64_t k = 0; k < n; ++k)
+                acc -= (long double)col[n - k] * (X[i * N + k] + (kind == 3 && i > 0 ? X[(i - 1) * N + k] : 0.0L));
             r[i] = acc;
         }
         if (kind == 0) {
@@ -319,13 +390,14 @@ double or_normal(uint64_t* state) {
 /* Separable forcing grid  F[i][n] = sum_j a_j trig_j(k_j pi x_i) * t_n^{p_j}
  * (trig 0 = sin, 1 = cos, 2 = 1, 3 = x(1-x), 4 = 1-2x) with x_i = i*h (i = 1..cells-1) and
  * t_n = (n + t_shift) * tau, n = 1..N  -- the reference's evaluation points
- * (schemes.cpp:403-407 diffusion; :301-302 wave with t_shift = -1/2). */
-void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double t_shift,
+ * (schemes.cpp:403-407 diffusion; :301-302 wave with t_shift = -1/2; Scheme 2
+ * :184-186 with x_shift = -1/2, x = (i - 1/2) h). */
+void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double x_shift, double t_shift,
                       int nmodes, const double* a, const double* k, const double* p,
                       const int* trig, double* F) {
     const double pi = 3.14159265358979323846;
     for (uint64_t i = 1; i < cells; ++i) {
-        const double x = (double)i * h;
+        const double x = ((double)i + x_shift) * h;
         for (uint64_t n = 1; n <= N; ++n) {
             const double t = ((double)n + t_shift) * tau;
             double v = 0.0;

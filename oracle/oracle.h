@@ -7,12 +7,17 @@
 extern "C" {
 #endif
 
-enum { OR_ODE = 0, OR_WAVE = 2, OR_DIFFUSION = 3 };
+enum { OR_ODE = 0, OR_HYPER = 1, OR_WAVE = 2, OR_DIFFUSION = 3 };
 
 double or_power_step(uint64_t k, double p);
 void or_weights(double p, uint64_t count, double* out);
 void or_constants(int scheme, double gamma, double tau, double* mu, double* c);
 void or_col_s4(double gamma, uint64_t N, double h, double tau, double* col);
+void or_col_s2(double gamma, uint64_t N, double h, double tau, double* a, double* b);
+void or_rhs_s2(double gamma, uint64_t cells, uint64_t N, double tau, const double* F,
+               const double* u0, double* R);
+void or_direct_s2(double gamma, uint64_t cells, uint64_t N, double h, double tau,
+                  const double* F, const double* u0, double* U);
 void or_col_s3(double gamma, uint64_t N, double h, double tau, double* col);
 void or_col_ode(double gamma, uint64_t N, double tau, double* col);
 void or_rhs_s4(double gamma, uint64_t cells, uint64_t N, double tau, const double* F,
@@ -33,7 +38,7 @@ void or_march_ld(int kind, uint64_t nodes, uint64_t N, const double* col, double
 uint64_t or_splitmix64(uint64_t* state);
 double or_uniform(uint64_t* state);
 double or_normal(uint64_t* state);
-void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double t_shift,
+void or_forcing_modes(uint64_t cells, uint64_t N, double h, double tau, double x_shift, double t_shift,
                       int nmodes, const double* a, const double* k, const double* p,
                       const int* trig, double* F);
 void or_sine_grid(uint64_t cells, double h, double amp, double* out);

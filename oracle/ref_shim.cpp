@@ -37,11 +37,11 @@ struct Grids {
     const double* phi;
     std::size_t N;
     std::size_t cells;
-    double h, tau, tshift;
+    double h, tau, tshift, xshift;
 };
 
 std::size_t node_of(const Grids& g, double x) {
-    long i = std::lround(x / g.h);
+    long i = std::lround(x / g.h - g.xshift);
     if (i < 1) i = 1;
     if (i > (long)g.cells - 1) i = (long)g.cells - 1;
     return (std::size_t)i;
@@ -72,27 +72,37 @@ int ref_weights(int kind, double gamma, uint64_t count, double* out) {
     }
 }
 
-// scheme: 2 = DiffusionWave (Scheme 3), 3 = Diffusion (Scheme 4)
+// scheme: 1 = Hyperbolic (Scheme 2), 2 = DiffusionWave (Scheme 3), 3 = Diffusion (Scheme 4)
 // method: 2 = Direct, 3 = Fast.  F: node-major forcing grid at the scheme's
-// evaluation points (S4: (i h, n tau); S3: (i h, (n-1/2) tau)).
+// evaluation points (S4: (i h, n tau); S3: (i h, (n-1/2) tau); S2: ((i-1/2) h, n tau)).
+// u0: interior nodes x_1..x_{cells-1}, except Scheme 2: x_0..x_{cells-1}.
 int ref_solve(int scheme, int method, double gamma, uint64_t time_steps, uint64_t space_cells,
               double time_length, double space_length, const double* F, const double* u0,
               const double* phi, double tol, uint64_t restart, uint64_t max_iter, double* U,
               uint64_t* iterations, double* seconds) {
     try {
         ProblemSpec spec;
-        spec.scheme = scheme == 2 ? SchemeId::DiffusionWave : SchemeId::Diffusion;
+        spec.scheme = scheme == 1 ? SchemeId::Hyperbolic : scheme == 2 ? SchemeId::DiffusionWave : SchemeId::Diffusion;
         spec.gamma = gamma;
         spec.time_steps = time_steps;
         spec.space_cells = space_cells;
         spec.time_length = time_length;
         spec.space_length = space_length;
         auto g = std::make_shared<Grids>(Grids{F, u0, phi, time_steps, space_cells, spec.h(),
-                                               spec.tau(), scheme == 2 ? -0.5 : 0.0});
+                                               spec.tau(), scheme == 2 ? -0.5 : 0.0, scheme == 1 ? -0.5 : 0.0});
         spec.forcing = [g](double x, double t) {
             return g->F[(node_of(*g, x) - 1) * g->N + (step_of(*g, t) - 1)];
         };
-        if (u0) spec.initial_u0 = [g](double x) { return g->u0[node_of(*g, x) - 1]; };
+        if (u0 && scheme == 1) {
+            spec.initial_u0 = [g](double x) {
+                long i = std::lround(x / g->h);
+                if (i < 0) i = 0;
+                if (i > (long)g->cells - 1) i = (long)g->cells - 1;
+                return g->u0[i];
+            };
+        } else if (u0) {
+            spec.initial_u0 = [g](double x) { return g->u0[node_of(*g, x) - 1]; };
+        }
         if (phi) spec.initial_phi = [g](double x) { return g->phi[node_of(*g, x) - 1]; };
         SolverConfig cfg;
         if (tol > 0) cfg.tol = tol;

@@ -40,8 +40,9 @@ class DomainError(FractimeError, ValueError):
     pass
 
 
-class SchemeId(enum.IntEnum):  # reference schemes.hpp:182 (Hyperbolic not provided)
+class SchemeId(enum.IntEnum):  # reference schemes.hpp:182
     Ode = 0
+    Hyperbolic = 1      # Scheme 2 (transport, 0 < gamma < 1; <= 2048 interior nodes)
     DiffusionWave = 2
     Diffusion = 3
 

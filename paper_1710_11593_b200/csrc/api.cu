@@ -62,6 +62,8 @@ struct ft_plan {
     double h = 0, tau = 0;
     int rhs_mode = 0;
     bool custom = false;  // ft_setup_toeplitz plan (caller's columns, no RHS assembly)
+    bool stencil = false; // Scheme 2: history products and in-leaf history act on U_i + U_(i-1)
+    double* vsrc_d = nullptr;  // Scheme 2: V = U_i + U_(i-1) (product sources), rows x N
     int J = 1;
     int device = 0;
     std::vector<double> gamma;
@@ -101,6 +103,7 @@ struct ft_plan {
     double* kcoef_d = nullptr;    // single-CTA Dirichlet coefficients
     double* respg_d = nullptr;    // multi-slab space-time response tables
     double* resph_d = nullptr;
+    double* respw_d = nullptr;    // multi-slab phase-2 injection responses (leaf_wbuild)
     std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
     std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf
     double* dw_d = nullptr;       // direct weights [B][N]
@@ -135,7 +138,8 @@ double power_step(uint64_t k, double p) {  // weights.cpp:8-16
 
 int validate(const ft_problem& s) {  // schemes.cpp:58-78
     const bool wave = s.scheme == FT_SCHEME_WAVE;
-    if (s.scheme != FT_SCHEME_ODE && s.scheme != FT_SCHEME_WAVE && s.scheme != FT_SCHEME_DIFFUSION)
+    if (s.scheme != FT_SCHEME_ODE && s.scheme != FT_SCHEME_HYPERBOLIC && s.scheme != FT_SCHEME_WAVE &&
+        s.scheme != FT_SCHEME_DIFFUSION)
         return set_err(FT_EINVAL, "solve: unknown scheme");
     if (wave) {
         if (!(s.gamma > 1.0 && s.gamma < 2.0))
@@ -364,7 +368,10 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     FT_CUDA(cudaGetDevice(&p->device));
 
     const uint64_t N = p->N;
-    p->kind = z.scheme == FT_SCHEME_ODE ? SK_DIAG : z.scheme == FT_SCHEME_WAVE ? SK_UPWIND : SK_TRIDIAG;
+    p->kind = z.scheme == FT_SCHEME_ODE ? SK_DIAG
+              : (z.scheme == FT_SCHEME_WAVE || z.scheme == FT_SCHEME_HYPERBOLIC) ? SK_UPWIND
+                                                                               : SK_TRIDIAG;
+    p->stencil = z.scheme == FT_SCHEME_HYPERBOLIC;
     p->gamma.resize(count);
     p->mu.resize(count);
     p->c.resize(count);
@@ -385,6 +392,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         const double mu = std::pow(tau, -g) / std::tgamma(2.0 - g);
         double c = mu;
         if (p->scheme == FT_SCHEME_WAVE) c = std::pow(tau, -g) / std::tgamma(3.0 - g);
+        if (p->scheme == FT_SCHEME_HYPERBOLIC) c = std::pow(tau, -g) / (2.0 * std::tgamma(2.0 - g));
         if (p->scheme == FT_SCHEME_DIFFUSION) c = std::pow(tau, -g) / std::tgamma(2.0 - g);
         p->mu[b] = mu;
         p->c[b] = c;
@@ -405,7 +413,17 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         } else {
             // g_weights(gamma, N) (+1 spare for the RHS kernel)
             for (uint64_t k = 0; k <= N; ++k) wv[k] = power_step(k, 1.0 - g);
-            if (p->scheme == FT_SCHEME_DIFFUSION) {
+            if (p->scheme == FT_SCHEME_HYPERBOLIC) {
+                // assemble_scheme2_reordered (schemes.cpp:160-165): A~ is the column; the
+                // step is A~_0 U_i - B~_0 U_(i-1) = r and, since B~_j = -A~_j for j >= 1,
+                // the history acts on U_i + U_(i-1) (the plan's source stencil)
+                col[0] = 1.0 / h + c * wv[0];
+                for (uint64_t j = 1; j < N; ++j) col[j] = c * (wv[j] - wv[j - 1]);
+                pc.d = col[0];
+                pc.off = 1.0 / h - c * wv[0];  // B~_0 (either sign)
+                // direct path (schemes.cpp:215-217): w = c * (g[j-1] - g[j]), rounded as there
+                for (uint64_t j = 1; j < N; ++j) dw[b * N + j] = c * (wv[j - 1] - wv[j]);
+            } else if (p->scheme == FT_SCHEME_DIFFUSION) {
                 col[0] = 2.0 / (h * h) + c * wv[0];  // schemes.cpp:394-396
                 for (uint64_t j = 1; j < N; ++j) col[j] = c * (wv[j] - wv[j - 1]);
                 pc.d = col[0];
@@ -467,6 +485,10 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         }
     }
     p->P_local = p->P;
+    if (p->stencil && p->multi) {
+        delete p;
+        return set_err(FT_EINVAL, "ft_setup: the hyperbolic scheme supports at most 2048 interior nodes per problem");
+    }
     if (world > 1) {
         if (!p->multi || count != 1 || p->P % world != 0 || rank < 0 || rank >= world) {
             delete p;
@@ -507,7 +529,8 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         if ((rc = alloc_copy((void**)&p->cprime_d, cprime.data(), sizeof(double) * cprime.size()))) return rc;
         if ((rc = alloc_copy((void**)&p->den_d, den.data(), sizeof(double) * den.size()))) return rc;
     }
-    if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * B * nodes))) return rc;
+    if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * 2 * B * nodes))) return rc;
+    if (p->stencil && (rc = alloc_copy((void**)&p->vsrc_d, nullptr, sizeof(double) * rows_of(p) * N))) return rc;
     if (p->multi) {
         if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
         p->xsend_d = p->xch_d;
@@ -529,6 +552,21 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         }
         if ((rc = alloc_copy((void**)&p->respg_d, G.data(), sizeof(double) * G.size()))) return rc;
         if ((rc = alloc_copy((void**)&p->resph_d, H.data(), sizeof(double) * H.size()))) return rc;
+        // phase 2 as a matvec: tabulate the reduced recursion's response to unit carries
+        const uint64_t wsz = B * (uint64_t)p->P * 2 * p->L * 2 * p->P;
+        if ((rc = alloc_copy((void**)&p->respw_d, nullptr, sizeof(double) * wsz))) return rc;
+        {
+            LeafArgs wa{};
+            wa.nodes = nodes;
+            wa.slab = p->slab;
+            wa.P = p->P;
+            wa.pc = p->pc_d;
+            wa.lampow = p->lampow_d;
+            wa.lp_stride = p->lp_stride;
+            wa.resp_h = p->resph_d;
+            FT_CUDA(launch_leaf_wbuild(p->kind, p->L, wa, (int)B, p->respw_d, 0));
+            FT_CUDA(cudaDeviceSynchronize());
+        }
     } else if (p->kind == SK_TRIDIAG) {
         std::vector<double> kc(B * 2 * nodes);
         for (uint64_t b = 0; b < B; ++b)
@@ -607,6 +645,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
         if (op.kind == OP_LEAF) {
             LeafArgs a;
             a.X = X;
+            a.V = p->stencil ? p->vsrc_d : nullptr;
+            a.stencil = p->stencil ? 1 : 0;
             const bool defer = io && io->defer;
             a.src = (op.first && !defer) ? rhs : X;
             a.radd = defer ? io->rdev : nullptr;
@@ -636,6 +676,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.rows_pp = p->local_nodes;
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
+            a.resp_w = p->respw_d;
             a.dbg = g_leaf_dbg;
             a.dbg_clk = (g_leaf_dbg & 4) ? p->dbgclk_d : nullptr;
             a.bar = p->bar_d;
@@ -670,6 +711,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             const Level& lv = p->levels[op.level];
             MpArgs a;
             a.X = X;
+            a.U = p->stencil ? p->vsrc_d : X;
             a.rsrc = (op.first && !(io && io->defer)) ? rhs : X;
             a.N = N;
             a.lo = op.t0;
@@ -874,6 +916,12 @@ int ft_assemble_rhs(const ft_plan* p, ft_forcing_fn f, ft_initial_fn u0, ft_init
             const double u = u0 ? u0(x, user) : 0.0;
             const double ph = phi ? phi(x, user) : 0.0;
             double* r = rhs + ((uint64_t)b * p->nodes + (i - 1)) * N;
+            if (p->scheme == FT_SCHEME_HYPERBOLIC) {  // Scheme2Rhs (schemes.cpp:176-187)
+                const double us = (u0 ? u0((double)i * h, user) : 0.0) + (u0 ? u0((double)(i - 1) * h, user) : 0.0);
+                const double x_half = ((double)i - 0.5) * h;
+                for (uint64_t n = 1; n <= N; ++n) r[n - 1] = f(x_half, (double)n * tau, user) + c * w[n - 1] * us;
+                continue;
+            }
             for (uint64_t n = 1; n <= N; ++n) {
                 if (p->scheme == FT_SCHEME_WAVE) {
                     const double t_half = ((double)n - 0.5) * tau;
@@ -906,6 +954,12 @@ int ft_assemble_rhs_grid(const ft_plan* p, const double* F, const double* u0, co
             const double ph = phi ? phi[row] : 0.0;
             const double* Fr = F + row * N;
             double* r = rhs + row * N;
+            if (p->scheme == FT_SCHEME_HYPERBOLIC) {  // u0 holds x_0..x_{cells-1} per problem
+                const double* ub = u0 ? u0 + (uint64_t)b * (p->nodes + 1) : nullptr;
+                const double us = ub ? ub[i + 1] + ub[i] : 0.0;
+                for (uint64_t n = 1; n <= N; ++n) r[n - 1] = Fr[n - 1] + c * w[n - 1] * us;
+                continue;
+            }
             for (uint64_t n = 1; n <= N; ++n) {
                 if (p->scheme == FT_SCHEME_WAVE) {
                     double value = Fr[n - 1] + c * tau * w[n - 1] * ph;
@@ -1114,6 +1168,8 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
         da.den = p->den_d;
         da.pc = p->pc_d;
         da.scratch = p->scratch_d;
+        da.scratch2 = p->scratch_d + (uint64_t)p->B * p->nodes;
+        da.stencil = p->stencil ? 1 : 0;
         FT_CUDA(launch_direct(da, p->B, st));
         launches = 1;
     }
@@ -1224,7 +1280,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);

@@ -5,6 +5,7 @@
 //
 //   Scheme 4 direct : src/schemes.cpp:434-463  (history :447-449, Thomas :453-461)
 //   Scheme 3 direct : src/schemes.cpp:333-352  (history :336-343, upwind march :345-351)
+//   Scheme 2 direct : src/schemes.cpp:210-232  (history :212-218, upwind march :219-228)
 //   ODE direct      : src/toeplitz.cpp:169-186 (lower_toeplitz_forward_solve)
 //   RHS             : src/schemes.cpp:401-408 (Scheme 4), :300-306 (Scheme3Rhs)
 #include "internal.cuh"
@@ -28,6 +29,12 @@ __global__ void __launch_bounds__(1024) direct_kernel(DirectArgs a) {
                 double hist = 0.0;
                 for (uint64_t k = 0; k < n; ++k) hist += w[n - k] * xi[k];
                 rhs[i] = xi[n] + pc.c * hist;
+            } else if (a.kind == SK_UPWIND && a.stencil) {
+                // Scheme 2 (schemes.cpp:212-218): history += w * U(i,k), w = c (g[j-1] - g[j])
+                double hist = 0.0;
+                for (uint64_t k = 0; k < n; ++k) hist += w[n - k] * xi[k];
+                rhs[i] = xi[n] + hist;
+                a.scratch2[(uint64_t)pb * nodes + i] = hist;
             } else if (a.kind == SK_UPWIND) {
                 double hist = 0.0;
                 if (n >= 1) {
@@ -50,6 +57,17 @@ __global__ void __launch_bounds__(1024) direct_kernel(DirectArgs a) {
                 rhs[0] /= dn[0];
                 for (int i = 1; i < nodes; ++i) rhs[i] = (rhs[i] - off * rhs[i - 1]) / dn[i];
                 for (int i = nodes - 1; i-- > 0;) rhs[i] -= cp[i] * rhs[i + 1];
+            } else if (a.kind == SK_UPWIND && a.stencil) {
+                // schemes.cpp:219-228: (rhs + hist_i + hist_left - (c g0 - 1/h) u_left) / (c g0 + 1/h);
+                // pc.off = 1/h - c g0, so  - (c g0 - 1/h) u_left == + off u_left exactly
+                const double* hs = a.scratch2 + (uint64_t)pb * nodes;
+                double u_left = 0.0, hist_left = 0.0;
+                for (int i = 0; i < nodes; ++i) {
+                    const double value = (rhs[i] + hist_left + pc.off * u_left) / pc.d;
+                    hist_left = hs[i];
+                    rhs[i] = value;
+                    u_left = value;
+                }
             } else if (a.kind == SK_UPWIND) {
                 double u_left = 0.0;
                 for (int i = 0; i < nodes; ++i) {
@@ -82,7 +100,7 @@ __global__ void rhs_modes_kernel(RhsModesArgs a) {
         const uint64_t row = idx / a.N;
         const int pb = (int)(row / a.nodes);
         const int i = a.node_begin + (int)(row % a.nodes) + 1;
-        const double x = a.scheme == 0 ? 0.0 : (double)i * a.h;
+        const double x = a.scheme == 0 ? 0.0 : a.scheme == 1 ? ((double)i - 0.5) * a.h : (double)i * a.h;
         const double n = (double)(n0 + 1);
         const double t = a.scheme == 2 ? (n - 0.5) * a.tau : n * a.tau;
         double f = 0.0;
@@ -99,7 +117,12 @@ __global__ void rhs_modes_kernel(RhsModesArgs a) {
         const double c = a.cvals[pb];
         const double u0 = a.u0amp ? a.u0amp[pb] * (a.scheme == 0 ? 1.0 : sin(3.14159265358979323846 * x)) : 0.0;
         double v;
-        if (a.scheme == 2) {
+        if (a.scheme == 1) {  // Scheme2Rhs: c g_(n-1) (u0(x_i) + u0(x_(i-1)))
+            const double amp = a.u0amp ? a.u0amp[pb] : 0.0;
+            const double us = amp * sin(3.14159265358979323846 * ((double)i * a.h)) +
+                              amp * sin(3.14159265358979323846 * ((double)(i - 1) * a.h));
+            v = f + c * wv[n0] * us;
+        } else if (a.scheme == 2) {
             const double phi = a.phiamp ? a.phiamp[pb] * sin(3.14159265358979323846 * x) : 0.0;
             v = f + c * a.tau * wv[n0] * phi;
             if (n0 >= 1) v -= c * (wv[n0 - 1] - wv[n0]) * u0;

@@ -78,14 +78,18 @@ struct LeafArgs {
     int rows_pp;               // X rows per problem held by this plan
     const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
     const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
+    const double* resp_w;      // [B][P][2 (EL,ER)][L lag][2P source carries] injection responses
     int dbg;                   // diagnostics: bit0 skip phase 2, bit1 skip phase 3
     unsigned* bar;             // fused slab leaf: grid-barrier counter (zeroed per solve)
     unsigned bar_target;       // value the counter reaches when every CTA of this leaf arrived
     long long* dbg_clk;        // diagnostics: per-phase clock64 stamps of CTA 0 (null = off)
+    double* V;                 // Scheme 2 (single slab): V = U_i + U_(i-1) written next to U, else null
+    int stencil;               // Scheme 2: in-leaf history acts on U_i + U_(i-1)
 };
 
 struct MpArgs {
     double* X;
+    const double* U;           // source rows U[lo, mid) (== X; Scheme 2: V = U_i + U_(i-1))
     const double* rsrc;        // target R is read from here (== X except first touch)
     uint64_t N;
     uint64_t lo, mid, hi;      // source [lo, mid), target [mid, min(hi, N))
@@ -111,6 +115,8 @@ struct DirectArgs {
     const double* den;    // [B][nodes] Thomas denominators (S4)
     const ProblemConst* pc;
     double* scratch;      // [B][nodes]
+    double* scratch2;     // [B][nodes] (Scheme 2: per-node history of the current step)
+    int stencil;          // Scheme 2 (kind SK_UPWIND)
 };
 
 struct RhsModesArgs {
@@ -143,6 +149,7 @@ cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, i
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,
                         int threads, cudaStream_t st);
 cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double* W, cudaStream_t st);
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);

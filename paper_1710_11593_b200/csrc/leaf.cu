@@ -148,7 +148,7 @@ __device__ __forceinline__ void store_rows(double* X, const double* src, uint64_
 template <int KIND, int NPT>
 __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanConsts<NPT>& sc,
                                          double (*s_wt)[2], int lane, int w, double (&Fv)[NPT],
-                                         double (&Bv)[NPT], double& totF, double& totB) {
+                                         double (&Bv)[NPT], double& totF, double& totB, double& Fpv) {
     constexpr int nw = kLeafThreads / 32;
     constexpr bool TRI = KIND == SK_TRIDIAG;
     double f[NPT], bl[NPT];
@@ -197,6 +197,7 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
     totF = runF;
     totB = runB;
     const double Fprev = fma(sc.lamLaneF, CF, exF);
+    Fpv = Fprev;  // F at the node before this thread's first node (0 before node 0)
 #pragma unroll
     for (int v = 0; v < NPT; ++v) Fv[v] = fma(sc.lamv1[v], Fprev, f[v]);
     if (TRI) {
@@ -280,6 +281,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     for (int k = 0; k < len; ++k) {
         const int par = k & 1;
         double x[NPT];
+        double xleft = 0.0;  // upwind: solution at the node left of this thread's first node
         if (KIND == SK_DIAG) {
 #pragma unroll
             for (int v = 0; v < NPT; ++v) x[v] = tile[v][0] / pc.d;
@@ -288,7 +290,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 #pragma unroll
             for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] / pc.d : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
-            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB);
+            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB, xleft);
             double cF = totF;
             if (padded) {  // F at the last real node (padding nodes carry zeros)
                 if (tid == own_t) {
@@ -317,8 +319,13 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         for (int v = 0; v < NPT; ++v) {
             x[v] *= vmask[v];  // padding nodes stay exactly zero
             outp[v * (L + 1)] = x[v];
+        }
 #pragma unroll
-            for (int i = 0; i + 1 < L; ++i) tile[v][i] = fma(-cw[i + 1], x[v], tile[v][i + 1]);
+        for (int v = NPT - 1; v >= 0; --v) {
+            // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
+            const double xs = a.stencil ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
+#pragma unroll
+            for (int i = 0; i + 1 < L; ++i) tile[v][i] = fma(-cw[i + 1], xs, tile[v][i + 1]);
             tile[v][L - 1] = 0.0;
         }
         ++outp;
@@ -328,6 +335,13 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     if (stamp) a.dbg_clk[10] = clock64();
     // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
     if (write_x) store_rows<L>(a.X, s_out, rowb, N, a.t0, mreal, len, tid, blockDim.x);
+    if (MODE == 0 && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1) (single-slab problems)
+        for (int e = tid; e < mreal * len; e += blockDim.x) {
+            const int q = e / len, k = e - q * len;
+            const double up = q > 0 ? s_out[(q - 1) * (L + 1) + k] : 0.0;
+            a.V[(rowb + q) * N + a.t0 + k] = s_out[q * (L + 1) + k] + up;
+        }
+    }
     if (MODE == 1) {
         double* xo = a.xsend + (uint64_t)cta * L * 2;
         for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
@@ -341,33 +355,169 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     leaf_body<KIND, NPT, L, MODE>(a, s_dyn0, true);
 }
 
-// Phase 2 + 3 of the slab decomposition (see file header).  One CTA per slab;
-// phase 2 runs on the first ceil(P/32) warps (one slab per lane) and is
-// replayed redundantly by every CTA (no second exchange).
+// Phase 2 reduced recursion (see file header): warps < ceil(P/32) of the
+// calling CTA, one slab per lane; `cin(sl, k, side)` supplies slab sl's
+// phase-1 carry of step k, `out(sl, k, EL, ER)` receives every active slab's
+// injections.  Used once per plan with unit impulses to tabulate the
+// injection response W (leaf_wbuild below); the per-leaf phase 2 is then a
+// matvec with W (correct_body).  Exact linear superposition of this recursion.
+template <int KIND, int L, class Cin, class Out>
+__device__ __forceinline__ void phase2_rec(const LeafArgs& a, int pb, int len, const double (*s_h)[L][4],
+                                           double (*s_part)[8][2], double* s_tot, Cin cin, Out out) {
+    constexpr bool TRI = KIND == SK_TRIDIAG;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int P = a.P;
+    const int nw2 = (P + 31) >> 5;
+    const ProblemConst pc = a.pc[pb];
+    const double lam = pc.lam;
+    const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
+    const int m = a.slab;
+    const int mlast = a.nodes - (P - 1) * m;
+    const int sl = w * 32 + lane;          // slab owned by this lane
+    const bool act = sl < P;
+    const int ht = (sl == P - 1) ? 1 : 0;  // response table of this slab
+    const double mu = lp[min(m, a.lp_stride - 1)];          // lam^m between slab ends
+    const double mu_last = lp[min(mlast, a.lp_stride - 1)];
+    double pw[5], pwb[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const double p = lp[min(m << d, a.lp_stride - 1)];
+        pw[d] = lane >= (1 << d) ? p : 0.0;
+        pwb[d] = lane + (1 << d) < 32 ? p : 0.0;
+    }
+    const double muW = lp[min(32 * m, a.lp_stride - 1)];
+    const double exm = lane > 0 ? 1.0 : 0.0, exbm = lane < 31 ? 1.0 : 0.0;
+    const double lamA = act ? lp[min(sl * m + 1, a.lp_stride - 1)] : 0.0;
+    const int last_s = act ? min(sl * m + m, a.nodes) - 1 : 0;
+    const double lamB = act ? lp[min(a.nodes - last_s, a.lp_stride - 1)] : 0.0;
+    const double lmF = lp[min(m * lane, a.lp_stride - 1)];
+    const double lmB = lp[min(m * (31 - lane), a.lp_stride - 1)];
+    // rolling accumulators: accF[i], accB[i] collect the lag responses
+    // destined for step k + i
+    double accF[L], accB[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        accF[i] = 0.0;
+        accB[i] = 0.0;
+    }
+    const int nth2 = nw2 * 32;
+#pragma unroll 2
+    for (int k = 0; k < len; ++k) {
+        double cF = act ? cin(sl, k, 0) + accF[0] : 0.0;
+        double cB = act ? cin(sl, k, 1) + accB[0] : 0.0;
+        // inclusive scans over slabs (uniform multiplier lam^m)
+        double SF = cF, SB = cB;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            SF = fma(pw[d], __shfl_up_sync(0xffffffffu, SF, 1 << d), SF);
+            if (TRI) SB = fma(pwb[d], __shfl_down_sync(0xffffffffu, SB, 1 << d), SB);
+        }
+        const double exF = exm * __shfl_up_sync(0xffffffffu, SF, 1);
+        const double exB = TRI ? exbm * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
+        double (*part)[2] = s_part[k & 1];
+        if (lane == 31) part[w][0] = SF;
+        if (lane == 0) part[w][1] = SB;
+        asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
+        double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
+        for (int ww = 0; ww < nw2; ++ww) {
+            if (ww == w) CF = runF;
+            runF = fma(muW, runF, part[ww][0]);
+            if (TRI) {
+                const int wb = nw2 - 1 - ww;
+                if (wb == w) CB = runB;
+                runB = fma(muW, runB, part[wb][1]);
+            }
+        }
+        // exclusive carries into this slab: F at the node before it, B after it
+        const double FLin = fma(lmF, CF, exF);
+        const double BRin = TRI ? fma(lmB, CB, exB) : 0.0;
+        double* tot = s_tot;
+        if (sl == P - 1) tot[0] = fma(mu_last, FLin, cF);  // F at node n-1
+        if (sl == 0) tot[1] = fma(mu, BRin, cB);            // B at node 0
+        asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
+        double EL, ER;
+        if (TRI) {
+            const double p0 = pc.G0 * lam * tot[1], pM1 = pc.G0 * lam * tot[0];
+            const double alpha = (pc.Lam * pM1 - p0) * pc.inv1mL2;
+            const double gam = (pc.Lam * p0 - pM1) * pc.inv1mL2;
+            EL = fma(pc.G0 * lam, FLin, alpha * lamA);
+            ER = fma(pc.G0 * lam, BRin, gam * lamB);
+        } else {
+            EL = lam * FLin;
+            ER = 0.0;
+        }
+        if (act) out(sl, k, EL, ER);
+#pragma unroll
+        for (int c = 0; c < L; c += 8) {
+            if (c == 0 || k + 1 + c < len) {  // dead entries (k + 1 + i >= len) skipped in chunks
+#pragma unroll
+                for (int i = c; i < c + 8 && i + 1 < L; ++i) {
+                    const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
+                    accF[i] = fma(hF.x, EL, fma(hF.y, ER, accF[i + 1]));
+                    if (TRI) {
+                        const double2 hB = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][2]);
+                        accB[i] = fma(hB.x, EL, fma(hB.y, ER, accB[i + 1]));
+                    }
+                }
+            }
+        }
+        accF[L - 1] = 0.0;
+        accB[L - 1] = 0.0;
+        // s_tot / s_part are rewritten next step only after its first barrier,
+        // which every reader of this step has passed
+    }
+}
+
+// Injection response table W[b][s][side][lag][j] (j = 2 s' + side'): slab s's
+// injection (EL: side 0, ER: side 1) at step `lag` caused by a unit phase-1
+// carry of slab s' (F: side' 0, B: side' 1) at step 0.  The reduced system is
+// time-invariant inside a leaf, so EL/ER_k = sum_{l<=k} sum_j W[.][k-l][j] c_l[j].
+// Grid (2P, B), block ceil(P/32) warps.
+template <int KIND, int L>
+__global__ void __launch_bounds__(kMaxSlabs / 32 * 32 + 32) leaf_wbuild(LeafArgs a, double* W) {
+    __shared__ __align__(16) double s_h[2][L][4];
+    __shared__ double s_part[2][8][2];
+    __shared__ double s_tot[2];
+    const int j = blockIdx.x, pb = blockIdx.y;
+    const int P = a.P;
+    const double* hsrc = a.resp_h + (uint64_t)pb * 2 * L * 4;
+    for (int i = threadIdx.x; i < 2 * L * 4; i += blockDim.x) (&s_h[0][0][0])[i] = hsrc[i];
+    __syncthreads();
+    const int js = j >> 1, jside = j & 1;
+    double* Wb = W + (uint64_t)pb * P * 2 * L * 2 * P;
+    phase2_rec<KIND, L>(
+        a, pb, L, s_h, s_part, s_tot,
+        [&](int sl, int k, int side) { return (sl == js && k == 0 && side == jside) ? 1.0 : 0.0; },
+        [&](int sl, int k, double EL, double ER) {
+            Wb[(((uint64_t)sl * 2 + 0) * L + k) * 2 * P + j] = EL;
+            Wb[(((uint64_t)sl * 2 + 1) * L + k) * 2 * P + j] = ER;
+        });
+}
+
+// Phase 2 + 3 of the slab decomposition (see file header).  One CTA per slab.
+// Phase 2 is a matvec with the tabulated injection response (leaf_wbuild):
+// every thread owns source carries j, accumulates the 2 x L injections of its
+// own slab over them, and a butterfly reduce-scatter + cross-warp sum folds
+// the 256 partial vectors (fixed order: bitwise reproducible, independent of
+// how slabs are partitioned over ranks).
 template <int KIND, int NPT, int L>
 __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, double* s_x, bool x_resident) {
-    // s_c0: [P][L][2] phase-1 carries of every slab; s_x: [m][L+1] phase-1 solution tile
-    __shared__ double s_h[2][L][4];         // lag responses (main slab, last slab): hFL hFR hBL hBR
+    // s_c0: carries of every slab transposed to [L][2P + 1]; s_x: [m][L+1] phase-1 solution tile
     __shared__ double s_inj[L][2];          // this slab's EL_k, ER_k
-    __shared__ double s_part[2][8][2];      // cross-warp scan partials (double buffered)
-    __shared__ double s_tot[2];             // F_M, B_1
+    __shared__ double s_red[kLeafThreads / 32][2 * L];
 
     constexpr bool TRI = KIND == SK_TRIDIAG;
     const int cta = blockIdx.x;
     const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int P = a.P;
-    const int nw2 = (P + 31) >> 5;          // phase-2 warps
-    const ProblemConst pc = a.pc[pb];
-    const double lam = pc.lam;
-    const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
     const int len = a.len;
     const int m = a.slab;
-    const int mlast = a.nodes - (P - 1) * m;
+    const int JS = 2 * P + 1;
 
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
     if (stamp) a.dbg_clk[0] = clock64();
-    // load the carries of every slab of this problem and the response tables
+    // load the carries of every slab of this problem (transposed) and the phase-1 tile
     const double* xin = a.xch + (uint64_t)pb * P * L * 2;
     for (int i0 = 0; i0 < P * L * 2; i0 += 8 * kLeafThreads) {  // 8 loads in flight per thread
         double v[8];
@@ -379,28 +529,24 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = i0 + u * kLeafThreads + tid;
-            if (i < P * L * 2) s_c0[i] = v[u];
+            if (i < P * L * 2) {
+                const int sp = i / (2 * L), r = i - sp * 2 * L;  // r = 2 l + side
+                s_c0[(r >> 1) * JS + 2 * sp + (r & 1)] = v[u];
+            }
         }
     }
-    const double* hsrc = a.resp_h + (uint64_t)pb * 2 * L * 4;
-    for (int i = tid; i < 2 * L * 4; i += blockDim.x) (&s_h[0][0][0])[i] = hsrc[i];
-    __syncthreads();
-
     const int slab0 = s * m;
     const int mreal = min(m, a.nodes - slab0);
     const uint64_t rowb = (uint64_t)pb * a.rows_pp + (slab0 - a.node_begin);  // X row of node slab0
-    if (stamp) a.dbg_clk[1] = clock64();
-    // ---- warps >= nw2 stage the phase-1 tile for phase 3 while phase 2 runs ----
-    if (w >= nw2 && !x_resident) {
-        const int nth = (kLeafThreads / 32 - nw2) * 32, me = tid - nw2 * 32;
+    if (!x_resident) {
         constexpr int HL = L / 2;
         const bool vec = len == L && (a.N & 1) == 0 && (a.t0 & 1) == 0;
         const int total = vec ? mreal * HL : mreal * len;
-        for (int e0 = 0; e0 < total; e0 += 8 * nth) {
+        for (int e0 = 0; e0 < total; e0 += 8 * kLeafThreads) {
             double2 v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int e = e0 + u * nth + me;
+                const int e = e0 + u * kLeafThreads + tid;
                 if (vec) {
                     const int q = e / HL, k2 = e - q * HL;
                     v[u] = e < total ? __ldcg(reinterpret_cast<const double2*>(a.X + (rowb + q) * a.N + a.t0) + k2)
@@ -412,7 +558,7 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int e = e0 + u * nth + me;
+                const int e = e0 + u * kLeafThreads + tid;
                 if (e >= total) continue;
                 if (vec) {
                     const int q = e / HL, k2 = e - q * HL;
@@ -425,109 +571,52 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
             }
         }
     }
-    // ---- phase 2: reduced recursion (warps < nw2, lane <-> slab) ----
-    if (w < nw2 && !(a.dbg & 1)) {
-        const int sl = w * 32 + lane;          // slab owned by this lane
-        const bool act = sl < P;
-        const int ht = (sl == P - 1) ? 1 : 0;  // response table of this slab
-        const double mu = lp[min(m, a.lp_stride - 1)];          // lam^m between slab ends
-        const double mu_last = lp[min(mlast, a.lp_stride - 1)];
-        double pw[5], pwb[5];
+    __syncthreads();
+    if (stamp) a.dbg_clk[1] = clock64();
+
+    // ---- phase 2: EL/ER_k = sum_{l<=k} sum_j W[k-l][j] c_l[j] ----
+    if (!(a.dbg & 1)) {
+        double acc[2 * L];  // [side][k]
 #pragma unroll
-        for (int d = 0; d < 5; ++d) {
-            const double p = lp[min(m << d, a.lp_stride - 1)];
-            pw[d] = lane >= (1 << d) ? p : 0.0;
-            pwb[d] = lane + (1 << d) < 32 ? p : 0.0;
-        }
-        const double muW = lp[min(32 * m, a.lp_stride - 1)];
-        const double exm = lane > 0 ? 1.0 : 0.0, exbm = lane < 31 ? 1.0 : 0.0;
-        const double lamA = act ? lp[min(sl * m + 1, a.lp_stride - 1)] : 0.0;
-        const int last_s = act ? min(sl * m + m, a.nodes) - 1 : 0;
-        const double lamB = act ? lp[min(a.nodes - last_s, a.lp_stride - 1)] : 0.0;
-        const double lmF = lp[min(m * lane, a.lp_stride - 1)];
-        const double lmB = lp[min(m * (31 - lane), a.lp_stride - 1)];
-        // rolling accumulators: accF[i], accB[i] collect the lag responses
-        // destined for step k + i
-        double accF[L], accB[L];
+        for (int o = 0; o < 2 * L; ++o) acc[o] = 0.0;
+        const double* Ws = a.resp_w + ((uint64_t)pb * P + s) * 2 * L * 2 * P;
+        for (int j = tid; j < 2 * P; j += kLeafThreads) {
 #pragma unroll
-        for (int i = 0; i < L; ++i) {
-            accF[i] = 0.0;
-            accB[i] = 0.0;
-        }
-        const int nth2 = nw2 * 32;
-#pragma unroll 2
-        for (int k = 0; k < len; ++k) {
-            double cF = act ? s_c0[(sl * L + k) * 2] + accF[0] : 0.0;
-            double cB = act ? s_c0[(sl * L + k) * 2 + 1] + accB[0] : 0.0;
-            // inclusive scans over slabs (uniform multiplier lam^m)
-            double SF = cF, SB = cB;
+            for (int side = 0; side < (TRI ? 2 : 1); ++side) {
+                double wv[L];
 #pragma unroll
-            for (int d = 0; d < 5; ++d) {
-                SF = fma(pw[d], __shfl_up_sync(0xffffffffu, SF, 1 << d), SF);
-                if (TRI) SB = fma(pwb[d], __shfl_down_sync(0xffffffffu, SB, 1 << d), SB);
-            }
-            const double exF = exm * __shfl_up_sync(0xffffffffu, SF, 1);
-            const double exB = TRI ? exbm * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
-            double (*part)[2] = s_part[k & 1];
-            if (lane == 31) part[w][0] = SF;
-            if (lane == 0) part[w][1] = SB;
-            asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
-            double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
-            for (int ww = 0; ww < nw2; ++ww) {
-                if (ww == w) CF = runF;
-                runF = fma(muW, runF, part[ww][0]);
-                if (TRI) {
-                    const int wb = nw2 - 1 - ww;
-                    if (wb == w) CB = runB;
-                    runB = fma(muW, runB, part[wb][1]);
+                for (int l = 0; l < L; ++l) wv[l] = __ldg(&Ws[((uint64_t)side * L + l) * 2 * P + j]);
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const double cv = l < len ? s_c0[l * JS + j] : 0.0;
+#pragma unroll
+                    for (int k = l; k < L; ++k) acc[side * L + k] = fma(wv[k - l], cv, acc[side * L + k]);
                 }
             }
-            // exclusive carries into this slab: F at the node before it, B after it
-            const double FLin = fma(lmF, CF, exF);
-            const double BRin = TRI ? fma(lmB, CB, exB) : 0.0;
-            double* tot = s_tot;
-            if (sl == P - 1) tot[0] = fma(mu_last, FLin, cF);  // F at node n-1
-            if (sl == 0) tot[1] = fma(mu, BRin, cB);            // B at node 0
-            asm volatile("bar.sync 1, %0;" ::"r"(nth2) : "memory");
-            double EL, ER;
-            if (TRI) {
-                const double p0 = pc.G0 * lam * tot[1], pM1 = pc.G0 * lam * tot[0];
-                const double alpha = (pc.Lam * pM1 - p0) * pc.inv1mL2;
-                const double gam = (pc.Lam * p0 - pM1) * pc.inv1mL2;
-                EL = fma(pc.G0 * lam, FLin, alpha * lamA);
-                ER = fma(pc.G0 * lam, BRin, gam * lamB);
-            } else {
-                EL = lam * FLin;
-                ER = 0.0;
-            }
-            if (!act) {
-                EL = 0.0;
-                ER = 0.0;
-            }
-            if (sl == s) {
-                s_inj[k][0] = EL;
-                s_inj[k][1] = ER;
-            }
-            if (a.dbg & 8) continue;  // timing ablation only (wrong results)
-#pragma unroll
-            for (int c = 0; c < L; c += 8) {
-                if (c == 0 || k + 1 + c < len) {  // dead entries (k + 1 + i >= len) skipped in chunks
-#pragma unroll
-                    for (int i = c; i < c + 8 && i + 1 < L; ++i) {
-                        const double2 hF = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][0]);
-                        accF[i] = fma(hF.x, EL, fma(hF.y, ER, accF[i + 1]));
-                        if (TRI) {
-                            const double2 hB = *reinterpret_cast<const double2*>(&s_h[ht][i + 1][2]);
-                            accB[i] = fma(hB.x, EL, fma(hB.y, ER, accB[i + 1]));
-                        }
-                    }
-                }
-            }
-            accF[L - 1] = 0.0;
-            accB[L - 1] = 0.0;
-            // s_tot / s_part are rewritten next step only after its first barrier,
-            // which every reader of this step has passed
         }
+        // butterfly reduce-scatter over the warp: lane keeps outputs 2 lane, 2 lane + 1
+#pragma unroll
+        for (int st = 0; st < 5; ++st) {
+            const int off = 16 >> st, half = L >> st;
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                const double send = up ? acc[i] : acc[i + half];
+                const double keep = up ? acc[i + half] : acc[i];
+                acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        s_red[w][2 * lane] = acc[0];
+        s_red[w][2 * lane + 1] = acc[1];
+        __syncthreads();
+        if (tid < 2 * L) {
+            double v = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kLeafThreads / 32; ++ww) v += s_red[ww][tid];
+            s_inj[tid & (L - 1)][tid / L] = v;
+        }
+    } else if (tid < 2 * L) {
+        s_inj[tid & (L - 1)][tid / L] = 0.0;
     }
     __syncthreads();
 
@@ -566,7 +655,7 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
 template <int KIND, int NPT, int L>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
-    correct_body<KIND, NPT, L>(a, s_dyn, s_dyn + (uint64_t)a.P * L * 2, false);
+    correct_body<KIND, NPT, L>(a, s_dyn, s_dyn + (uint64_t)L * (2 * a.P + 1), false);
 }
 
 // Single-GPU slab leaf in ONE cooperative kernel: phase 1, publish carries, a
@@ -575,7 +664,7 @@ template <int KIND, int NPT, int L>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
     double* s_c0 = s_dyn;
-    double* s_x = s_dyn + (uint64_t)a.P * L * 2;
+    double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
     leaf_body<KIND, NPT, L, 1>(a, s_x, false);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -612,11 +701,11 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st) {
-    const size_t smem = sizeof(double) * ((size_t)a.P * L * 2 + (size_t)a.slab * (L + 1));
+    const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)a.slab * (L + 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(leaf_correct<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * (kMaxSlabs * L * 2 + kLeafThreads * NPT * (L + 1))));
+                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
     leaf_correct<KIND, NPT, L><<<ctas, kLeafThreads, smem, st>>>(a);
@@ -625,11 +714,11 @@ static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st
 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) {
-    const size_t smem = sizeof(double) * ((size_t)a.P * L * 2 + (size_t)kLeafThreads * NPT * (L + 1));
+    const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(leaf_fused<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * (kMaxSlabs * L * 2 + kLeafThreads * NPT * (L + 1))));
+                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
     void* args[] = {(void*)&a};
@@ -651,6 +740,16 @@ cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int
         if (kind == SK_UPWIND) return launch_correct_t<SK_UPWIND, 2, 32>(a, ctas, st);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double* W, cudaStream_t st) {
+    const dim3 grid(2 * a.P, B);
+    const int threads = ((a.P + 31) / 32) * 32;
+    if (L != 32) return cudaErrorInvalidValue;
+    if (kind == SK_TRIDIAG) leaf_wbuild<SK_TRIDIAG, 32><<<grid, threads, 0, st>>>(a, W);
+    else if (kind == SK_UPWIND) leaf_wbuild<SK_UPWIND, 32><<<grid, threads, 0, st>>>(a, W);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
 }
 
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st) {

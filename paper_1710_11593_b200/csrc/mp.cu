@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     for (int t = threadIdx.x; t < total / 16; t += blockDim.x) {
         const int g = t / Q0, j = t - g * Q0;
         const PairInfo pi = s_pair[g];
-        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        const double* x1 = a.U + pi.row1 * N + a.lo + j;
         const bool live = pair0 + g < npairs;
         cplx v[16];
 #pragma unroll
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
                 const int tp = (int)(t - a.mid);
                 if (tp < a.J - 1) {  // exact near field: lags t - j < J
                     const double* cp = a.col + (uint64_t)pi.pb * N;
-                    const double* x1 = a.X + row1 * N;
+                    const double* x1 = a.U + row1 * N;
                     const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
                     double s1 = 0.0, s2 = 0.0;
                     for (uint64_t j = a.mid; j-- > jlo;) {
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
         const int tp = (int)(t - a.mid);
         if (tp < a.J - 1) {
             const double* cp = a.col + (uint64_t)pb * N;
-            const double* x1 = a.X + row1 * N;
+            const double* x1 = a.U + row1 * N;
             const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
             double s1 = 0.0, s2 = 0.0;
             for (uint64_t j = a.mid; j-- > jlo;) {
@@ -386,7 +386,7 @@ __device__ __forceinline__ void mp1_last_task(const MpArgs& a, cplx* buf, const 
         const int tp = (int)(tt - a.mid);
         if (tp < a.J - 1) {  // exact near field: lags t - j < J
             const double* cp = a.col + (uint64_t)pi.pb * N;
-            const double* xr = a.X + pi.row1 * N;
+            const double* xr = a.U + pi.row1 * N;
             const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
             double s1 = 0.0, s2 = 0.0;
             for (uint64_t jj = a.mid; jj-- > jlo;) {
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kMpThreads, FT_MP1_MINB) mp1_kernel(MpArgs a) 
     for (int t = threadIdx.x; t < total / 16; t += kMpThreads) {
         const int g = t / Q0, j = t - g * Q0;
         const PairInfo pi = s_pair[g];
-        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        const double* x1 = a.U + pi.row1 * N + a.lo + j;
         const bool live = pair0 + g < npairs;
         cplx v[16];
 #pragma unroll
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
 
     // pass 0 (S = n, radix 16) from HBM; inputs p >= 8 are the zero padding
     {
-        const double* x1 = a.X + pi.row1 * N + a.lo + j;
+        const double* x1 = a.U + pi.row1 * N + a.lo + j;
         cplx v[16];
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
         const int tp = (int)(tt - a.mid);
         if (tp < a.J - 1) {  // exact near field: lags t - j < J
             const double* cp = a.col + (uint64_t)pi.pb * N;
-            const double* xr = a.X + pi.row1 * N;
+            const double* xr = a.U + pi.row1 * N;
             const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
             double s1 = 0.0, s2 = 0.0;
             for (uint64_t jj = a.mid; jj-- > jlo;) {
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
         const int r2 = e / H, j = e - r2 * H;
         const uint64_t row = row0 + r2;
         const bool ok = row < (uint64_t)a.rows;
-        uu[i] = ok ? a.X[row * N + a.lo + j] : 0.0;
+        uu[i] = ok ? a.U[row * N + a.lo + j] : 0.0;
         rv[i] = (ok && j < nt) ? a.rsrc[row * N + a.mid + j] : 0.0;
     }
 #pragma unroll

@@ -2,8 +2,8 @@
 
 Restates `run_convergence` / `exponent_ladder` / `emit_csv` / `emit_markdown`
 (reference proj/src/harness.cpp:135-164, 184-236, 296-316) for the schemes on
-this path (Example 3 = wave, Scheme 3; Example 4 = diffusion, Scheme 4,
-harness.cpp:69-86): manufactured solutions at h = 2^-e (tau = 2^-e, or a fixed
+this path (Example 2 = transport, Scheme 2; Example 3 = wave, Scheme 3;
+Example 4 = diffusion, Scheme 4, harness.cpp:58-86): manufactured solutions at h = 2^-e (tau = 2^-e, or a fixed
 tau = 2^-P), the final-time L2 error (`l2_error`, schemes.cpp:525-542), the
 rate between consecutive ladder levels, and the CSV header/columns the
 reference emits (`%.17g` doubles).  The forcing is generated on the device
@@ -25,7 +25,8 @@ import numpy as np
 from . import Plan, SchemeId, SolveMethod
 from . import workloads as W
 
-SCHEME_NAME = {SchemeId.DiffusionWave: "wave", SchemeId.Diffusion: "diffusion"}  # schemes.cpp:24-32
+SCHEME_NAME = {SchemeId.Hyperbolic: "hyperbolic", SchemeId.DiffusionWave: "wave",
+               SchemeId.Diffusion: "diffusion"}  # schemes.cpp:24-32
 HEADER = "mesh_exp,h,tau,l2_error,rate,iterations,wall_seconds,method,gamma,scheme"  # harness.cpp:297
 
 
@@ -62,8 +63,8 @@ def run_example(eid: int, gamma: float, exp: int, time_steps: int, cells: int,
     """harness.cpp:176-194 on the GPU: solve the manufactured problem, L2 error at t = T."""
     import torch
 
-    if eid not in (3, 4):
-        raise ValueError("example id must be 3 (wave) or 4 (diffusion) on this path")
+    if eid not in (2, 3, 4):
+        raise ValueError("example id must be 2 (transport), 3 (wave) or 4 (diffusion) on this path")
     w = _example(eid, gamma, time_steps, cells)
     plan = Plan(w.specs)
     rhs = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
@@ -121,7 +122,7 @@ def emit_markdown(rows: List[ConvergenceRow], out=None) -> str:
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
-    ap.add_argument("--example", type=int, required=True, choices=(3, 4))
+    ap.add_argument("--example", type=int, required=True, choices=(2, 3, 4))
     ap.add_argument("--gamma", type=float, nargs="+", required=True)
     ap.add_argument("--levels", default="3..8", help="exponent range A..B (mesh 2^-A .. 2^-B)")
     ap.add_argument("--fixed-tau-exp", type=int, default=None)

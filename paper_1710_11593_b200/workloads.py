@@ -73,9 +73,15 @@ class Workload:
 
 
 def example(eid: int, gamma: float, e: int) -> Workload:
-    """The reference's manufactured Examples 3 and 4 (proj/src/harness.cpp:69-86)
-    at h = tau = 2^-e, as used by its acceptance tables (acceptance.cpp:72-90)."""
+    """The reference's manufactured Examples 2, 3 and 4 (proj/src/harness.cpp:58-86)
+    at h = tau = 2^-e, as used by its acceptance tables (acceptance.cpp:62-90)."""
     n = 1 << e
+    if eid == 2:  # transport (Scheme 2), u = t sin(pi x), forcing at ((i - 1/2) h, n tau)
+        spec = ProblemSpec(SchemeId.Hyperbolic, gamma, n, n, 1.0, 1.0)
+        a = np.array([[1.0 / math.gamma(2.0 - gamma), math.pi]])
+        p = np.array([[1.0 - gamma, 1.0]])
+        return Workload(f"example2-e{e}", [spec], a, np.array([1.0, 1.0]), p, np.array([0, 1]), None, None,
+                        "t sin(pi x)")
     if eid == 4:  # diffusion, u = t^3 sin(pi x)
         spec = ProblemSpec(SchemeId.Diffusion, gamma, n, n, 1.0, 1.0)
         a = np.array([[6.0 / math.gamma(4.0 - gamma), math.pi ** 2]])
@@ -91,11 +97,27 @@ def example(eid: int, gamma: float, e: int) -> Workload:
     raise ValueError(eid)
 
 
+def transport(gamma: float, time_steps: int, cells: int, u0amp: Optional[float] = None) -> Workload:
+    """Scheme 2 (transport) test problem: Example 2's forcing (harness.cpp:58-67)
+    on an arbitrary mesh, optionally with u0 = u0amp sin(pi x) to exercise the
+    initial-data term of Scheme2Rhs (schemes.cpp:183-187)."""
+    w = example(2, gamma, 1)
+    s = w.specs[0]
+    s.time_steps, s.space_cells = time_steps, cells
+    w.name = f"transport-g{gamma}-n{time_steps}-c{cells}"
+    if u0amp is not None:
+        w.u0amp = np.array([float(u0amp)])
+        w.exact = None
+    return w
+
+
 def exact_final(w: Workload) -> np.ndarray:
     """Exact solution at t = T on the interior nodes (for the examples / configs)."""
     s = w.specs[0]
     x = np.arange(1, s.space_cells) * s.h()
     t = s.time_length
+    if w.exact == "t sin(pi x)":
+        return t * np.sin(np.pi * x)
     if w.exact == "t^3 sin(pi x)":
         return t ** 3 * np.sin(np.pi * x)
     if w.exact == "t^3 x (1-x)":

@@ -30,7 +30,7 @@ def parse_tables():
     """kDiffusionReference / kWaveReference from the reference acceptance test."""
     src = REF_ACCEPT.read_text()
     out = {}
-    for name in ("kDiffusionReference", "kWaveReference"):
+    for name in ("kDiffusionReference", "kWaveReference", "kTransportReference"):
         body = src[src.index(name):]
         body = body[:body.index("};")]
         cols = []
@@ -49,7 +49,14 @@ CASES = [  # (name, config, kwargs) -- small enough for the reference direct pat
     ("cfg3_m16_n128", 3, dict(time_steps=128, cells=17)),
     ("cfg4_m32_n64", 4, dict(time_steps=64, cells=33)),
     ("cfg4_m4096_n16", 4, dict(time_steps=16, cells=4097)),
+    ("s2_g0.5_n16_m8", "transport", dict(gamma=0.5, time_steps=16, cells=8)),
+    ("s2_g0.3_n64_m33_u0", "transport", dict(gamma=0.3, time_steps=64, cells=33, u0amp=1.0)),
+    ("s2_g0.9_n100_m20_u0", "transport", dict(gamma=0.9, time_steps=100, cells=20, u0amp=-0.7)),
 ]
+
+
+def case_workload(cid, kw):
+    return W.transport(**kw) if cid == "transport" else W.config(cid, **kw)
 
 
 def main():
@@ -65,7 +72,7 @@ def main():
     data["power_step_1e9_0.5"] = np.array([L.ref_power_step(1000000000, 0.5)])
     # solutions through the reference's public solve() / Toeplitz API
     for name, cid, kw in CASES:
-        w = W.config(cid, **kw)
+        w = case_workload(cid, kw)
         s = w.specs[0]
         F = oracle.forcing_grid(w)
         u0 = oracle.initial_grid(w, w.u0amp)

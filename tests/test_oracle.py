@@ -53,17 +53,25 @@ def test_weights_telescope(oracle_mod, gold, kind, gamma):
     assert np.array_equal(w, gold[key])
 
 
-CASES = ["cfg1_n256", "cfg2_m16_n128", "cfg2_m31_n100", "cfg3_m16_n128", "cfg4_m32_n64", "cfg4_m4096_n16"]
+CASES = ["cfg1_n256", "cfg2_m16_n128", "cfg2_m31_n100", "cfg3_m16_n128", "cfg4_m32_n64", "cfg4_m4096_n16",
+         "s2_g0.5_n16_m8", "s2_g0.3_n64_m33_u0", "s2_g0.9_n100_m20_u0"]
 CFG = {"cfg1_n256": (1, dict(time_steps=256)), "cfg2_m16_n128": (2, dict(time_steps=128, cells=17)),
        "cfg2_m31_n100": (2, dict(time_steps=100, cells=32)), "cfg3_m16_n128": (3, dict(time_steps=128, cells=17)),
-       "cfg4_m32_n64": (4, dict(time_steps=64, cells=33)), "cfg4_m4096_n16": (4, dict(time_steps=16, cells=4097))}
+       "cfg4_m32_n64": (4, dict(time_steps=64, cells=33)), "cfg4_m4096_n16": (4, dict(time_steps=16, cells=4097)),
+       "s2_g0.5_n16_m8": ("transport", dict(gamma=0.5, time_steps=16, cells=8)),
+       "s2_g0.3_n64_m33_u0": ("transport", dict(gamma=0.3, time_steps=64, cells=33, u0amp=1.0)),
+       "s2_g0.9_n100_m20_u0": ("transport", dict(gamma=0.9, time_steps=100, cells=20, u0amp=-0.7))}
+
+
+def case_workload(cid, kw):
+    return W.transport(**kw) if cid == "transport" else W.config(cid, **kw)
 
 
 @pytest.mark.parametrize("name", CASES)
 def test_oracle_bitwise_vs_reference_golden(oracle_mod, gold, name):
     """The restated direct march is bit-identical to the reference's solve(Direct)."""
     cid, kw = CFG[name]
-    w = W.config(cid, **kw)
+    w = case_workload(cid, kw)
     F = oracle_mod.forcing_grid(w)
     assert np.array_equal(F, gold[f"{name}_F"]), "forcing generator drifted"
     u0 = gold[f"{name}_u0"] if f"{name}_u0" in gold else None
@@ -78,29 +86,36 @@ def test_oracle_vs_live_reference(oracle_mod):
         pytest.skip("oracle/_ref not built")
     rng = np.random.default_rng(5)
     for cid, kw in [(2, dict(time_steps=40, cells=9)), (3, dict(time_steps=33, cells=12)),
-                    (4, dict(time_steps=17, cells=65))]:
-        w = W.config(cid, **kw)
+                    (4, dict(time_steps=17, cells=65)), ("transport", dict(gamma=0.4, time_steps=29, cells=13))]:
+        w = case_workload(cid, kw)
         F = rng.standard_normal((w.nodes, w.N))
-        u0 = rng.standard_normal(w.nodes)
+        u0 = rng.standard_normal(w.nodes + (1 if cid == "transport" else 0))
         phi = rng.standard_normal(w.nodes) if cid == 3 else None
         U = oracle_mod.direct(w, F, u0, phi)
         Ur, _, _ = oracle_mod.ref_solve(w.specs[0], "direct", F, u0, phi)
         assert np.array_equal(U, Ur)
 
 
-@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference")])
+@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference"),
+                                     (2, "kTransportReference")])
 def test_oracle_reproduces_paper_tables(oracle_mod, eid, key):
-    """The reference's frozen Example 3/4 L2 errors (acceptance.cpp:72-90) at
-    h = tau = 2^-3..2^-6, 5% tolerance and rates within 0.05 as the reference checks."""
+    """The reference's frozen Example 2/3/4 L2 errors (acceptance.cpp:62-90) at
+    h = 2^-3..2^-6 (tau = h; Example 2: tau = 2^-10 fixed, acceptance.cpp:242),
+    5% tolerance and rates within 0.05 as the reference checks.  The transport
+    column carries the reference's documented x10 scale defect (proj/README.md:92-96):
+    the measured errors equal one tenth of the frozen values."""
     tables = json.loads((GOLD / "tables.json").read_text())
+    scale = 0.1 if eid == 2 else 1.0
     for col in tables[key]:
         errs = []
         for e in range(3, 7):
             w = W.example(eid, col["gamma"], e)
+            if eid == 2:
+                w.specs[0].time_steps = 1 << 10
             U = oracle_mod.direct(w, oracle_mod.forcing_grid(w))
             errs.append(W.l2_final(w, U))
         for i, err in enumerate(errs):
-            assert abs(err - col["errors"][i]) <= 0.05 * col["errors"][i]
+            assert abs(err - scale * col["errors"][i]) <= 0.05 * scale * col["errors"][i]
         for i in range(1, len(errs)):
             assert abs(math.log2(errs[i - 1] / errs[i]) - col["rates"][i - 1]) <= 0.05
 
