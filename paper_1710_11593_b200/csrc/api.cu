@@ -85,6 +85,7 @@ struct ft_plan {
     unsigned* bar_d = nullptr;  // fused slab leaf grid barrier
     cplx* mpscratch_d = nullptr;  // split K-branch history products
     bool split_k = true;
+    int split_min_k = 8;        // K-branch levels with K >= this use the split (scratch) path
     long long* dbgclk_d = nullptr;
     bool fused_leaf = true;
     // levels
@@ -604,7 +605,8 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     }
     {
         bool needs = false;
-        for (auto& lv : p->levels) needs = needs || lv.K >= 8;
+        p->split_min_k = getenv("FT_SPLIT_MIN_K") ? atoi(getenv("FT_SPLIT_MIN_K")) : 8;  // tuning knob
+        for (auto& lv : p->levels) needs = needs || lv.K >= p->split_min_k;
         p->split_k = getenv("FT_CLUSTER_K") == nullptr;
         if (needs && p->split_k)
             if ((rc = alloc_copy((void**)&p->mpscratch_d, nullptr, kMpScratchBytes))) return rc;
@@ -729,7 +731,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.logT = p->logT;
             a.col = p->col_d;
             a.J = p->J;
-            a.scratch = (lv.K >= 8 && p->split_k) ? p->mpscratch_d : nullptr;  // K = 4: clusters measured faster
+            a.scratch = (lv.K >= p->split_min_k && p->split_k) ? p->mpscratch_d : nullptr;  // K = 4: clusters measured faster
             a.pair_begin = 0;
             a.pair_count = 0;
             FT_CUDA(launch_mp(a, lv.groups, st));

@@ -33,7 +33,8 @@ constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in 
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
 constexpr int kMpDirectMaxH = 64;   // blocks n <= 128 use the direct Toeplitz kernel
-constexpr int kMpSingleMaxN = 8192; // 256 <= n <= 8192: single-CTA n-point FFT kernel
+constexpr int kMpSingleMaxN = 4096; // 256 <= n <= 4096: single-CTA n-point FFT kernel (n = 8192 as a
+                                    // 2-CTA cluster: 32.0 vs 34.8 ms per level, 1 CTA/SM single)
 constexpr int kMpBranchMax = 4096;  // larger n: K-CTA clusters of (n / K)-point branches (8192 measured slower: 1 CTA/SM)
 
 struct __align__(16) cplx {

@@ -66,7 +66,7 @@ __device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
 // a.scratch and mpB_kernel performs the cross-branch combine (K >= 4 levels:
 // 16-CTA clusters packed badly -- 14 active clusters -- and stalled on
 // cluster barriers, ncu).
-template <int K, int LOGM, bool SPLIT>
+template <int K, int LOGM, bool SPLIT, bool FOLDED = false>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
@@ -106,6 +106,12 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
         const double* x1 = a.U + pi.row1 * N + a.lo + j;
         const bool live = pair0 + g < npairs;
         cplx v[16];
+        if constexpr (FOLDED) {
+            // branch input already folded + twisted by mp_fold_kernel (in place in scratch)
+            const cplx* in = a.scratch + ((uint64_t)(pair0 + g - a.pair_begin) * K + b) * m + j;
+#pragma unroll
+            for (int p = 0; p < 16; ++p) v[p] = ldgc(&in[(uint64_t)p * Q0]);
+        } else {
 #pragma unroll
         for (int p = 0; p < 16; ++p) v[p] = {0.0, 0.0};
 #pragma unroll
@@ -124,6 +130,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
             const cplx tj = conjc(ldgc(&a.tw[n + b * j]));  // theta_b^j
 #pragma unroll
             for (int p = 0; p < 16; ++p) v[p] = cmul(v[p], cmul(tj, s_tq[p]));
+        }
         }
         dft_reg<16, false>(v);
         cplx w[16];
@@ -249,6 +256,45 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
     }
     cluster.sync();
     }
+}
+
+// Pre-fold of the split K-branch levels (four-step first pass): thread <->
+// (pair, r), r < m.  Reads the K/2 source chunks x_q = U[lo + q m + r] of the
+// packed row pair once, forms every branch's input
+//     f_b(r) = theta_b^r sum_q x_q zeta_b^q,  zeta_b = e^(2 pi i b / K),  theta_b = e^(2 pi i b / n)
+// with one K-point DFT (upper half of the inputs is the zero padding), and
+// writes f_b to scratch[pair][b][r]; mp_kernel<.., FOLDED> then reads its
+// branch straight from there instead of re-reading and folding the whole
+// source block in every branch CTA (K-fold L2 traffic and K/2 complex MACs
+// per point, ncu).
+template <int K, int LOGM>
+__global__ void __launch_bounds__(kMpThreads) mp_fold_kernel(MpArgs a) {
+    constexpr int m = 1 << LOGM;
+    const int n = a.n;
+    const int pl = blockIdx.y;
+    const int rp = a.pair_begin + pl;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    if (rp >= npairs || r >= m) return;
+    const uint64_t N = a.N;
+    const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+    const int i1 = 2 * lp;
+    const bool has2 = i1 + 1 < a.nodes;
+    const uint64_t row1 = (uint64_t)(pb * a.nodes + i1);
+    const double* x1 = a.U + row1 * N + a.lo + r;
+    cplx v[K];
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) {
+        v[q].x = x1[(uint64_t)q * m];
+        v[q].y = has2 ? x1[N + (uint64_t)q * m] : 0.0;
+    }
+#pragma unroll
+    for (int q = K / 2; q < K; ++q) v[q] = {0.0, 0.0};
+    dft_reg<K, true>(v);  // v[b] = sum_q x_q e^(+2 pi i b q / K)
+    cplx* out = a.scratch + (uint64_t)pl * K * m + r;
+    out[0] = v[0];
+#pragma unroll
+    for (int bb = 1; bb < K; ++bb) out[(uint64_t)bb * m] = cmulc(v[bb], ldgc(&a.tw[n + bb * r]));
 }
 
 // Cross-branch combine of the split K-branch levels: thread <-> (pair, r):
@@ -858,22 +904,42 @@ __global__ void __launch_bounds__(kMpThreads) spectra_kernel(SpecArgs a) {
 
 size_t mp_smem_bytes(int G, int m) { return sizeof(cplx) * (size_t)spad_len(G * m); }
 
+static uint64_t split_batch_bytes() {
+    static const uint64_t b = [] {
+        const char* e = getenv("FT_MP_BATCH_MB");  // tuning knob (default: the whole scratch)
+        const uint64_t v = e ? (uint64_t)atoll(e) << 20 : kMpScratchBytes;
+        return std::min<uint64_t>(std::max<uint64_t>(v, 1ull << 20), kMpScratchBytes);
+    }();
+    return b;
+}
+
 template <int K, int LOGM>
 static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(mp_kernel<K, LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
+        cudaFuncSetAttribute(mp_kernel<K, LOGM, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
         attr_set = true;
     }
+    // pre-fold measured faster for K = 16 (n = 65536: 63.5 -> 52.0 ms per level), slower
+    // for K = 8 (42.8 -> 46.4 ms: the extra scratch round trip outweighs the K-fold re-reads)
+    static const int prefold_min_k = getenv("FT_PREFOLD_MIN_K") ? atoi(getenv("FT_PREFOLD_MIN_K")) : 16;
+    const bool prefold = K >= prefold_min_k && getenv("FT_NO_PREFOLD") == nullptr;
     constexpr int m = 1 << LOGM;
     const int npairs = (a0.rows / a0.nodes) * a0.pairs_per_problem;
-    const int batch = (int)std::max<uint64_t>(1, kMpScratchBytes / ((uint64_t)K * m * sizeof(cplx)));
+    const int batch = (int)std::max<uint64_t>(1, split_batch_bytes() / ((uint64_t)K * m * sizeof(cplx)));
     MpArgs a = a0;
     for (int p0 = 0; p0 < npairs; p0 += batch) {
         a.pair_begin = p0;
         a.pair_count = std::min(batch, npairs - p0);
-        mp_kernel<K, LOGM, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+        if (prefold) {
+            mp_fold_kernel<K, LOGM><<<dim3(m / kMpThreads, a.pair_count), kMpThreads, 0, st>>>(a);
+            mp_kernel<K, LOGM, true, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+        } else {
+            mp_kernel<K, LOGM, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         mpB_kernel<K, LOGM><<<dim3(m / kMpThreads, a.pair_count), kMpThreads, 0, st>>>(a);
@@ -923,7 +989,10 @@ static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
 }
 
 bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
-bool mp_is_single(int n) { return !mp_is_direct(n) && n >= 256 && n <= kMpSingleMaxN; }
+bool mp_is_single(int n) {
+    static const int single_max = getenv("FT_SINGLE_MAX") ? atoi(getenv("FT_SINGLE_MAX")) : kMpSingleMaxN;
+    return !mp_is_direct(n) && n >= 256 && n <= single_max;
+}
 
 template <int LOGN>
 static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
@@ -1005,6 +1074,7 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
     }
     const int key = a.K * 100 + (__builtin_ctz(a.m));
     switch (key) {
+        case 212: return launch_mp_k<2, 12>(a, groups, st);
         case 412: return launch_mp_k<4, 12>(a, groups, st);
         case 812: return launch_mp_k<8, 12>(a, groups, st);
         case 1612: return launch_mp_k<16, 12>(a, groups, st);

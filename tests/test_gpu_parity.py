@@ -263,3 +263,14 @@ def test_harness_convergence_tables(ft, eid, key):
         assert abs(r.rate - rate) <= 0.05
     csv = H.emit_csv(rows).splitlines()
     assert len(csv) == 7 and all(len(line.split(",")) == 10 for line in csv)
+
+
+@pytest.mark.parametrize("cid", [4, 3])
+def test_every_level_full_N(ft, oracle_mod, cid):
+    """Full N = 65536 on two nodes: every D&C level, including the n = 8192..65536
+    K-branch history products (cluster and split/pre-folded paths)."""
+    w = W.config(cid, cells=3)
+    F, u0, phi = _inputs(oracle_mod, w)
+    ref = oracle_mod.direct(w, F, u0, phi)
+    _, _, U, _ = _fast(ft, w, F, u0, phi)
+    assert oracle_mod.relerr(U, ref) <= TOL
