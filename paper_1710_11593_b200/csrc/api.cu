@@ -679,6 +679,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
             a.resp_w = p->respw_d;
+            a.pdl_trigger = pdl_mode() == 1;
             a.dbg = g_leaf_dbg;
             a.dbg_clk = (g_leaf_dbg & 4) ? p->dbgclk_d : nullptr;
             a.bar = p->bar_d;
@@ -714,6 +715,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             MpArgs a;
             a.X = X;
             a.U = p->stencil ? p->vsrc_d : X;
+            a.pdl_trigger = pdl_mode() == 1;
             a.rsrc = (op.first && !(io && io->defer)) ? rhs : X;
             a.N = N;
             a.lo = op.t0;

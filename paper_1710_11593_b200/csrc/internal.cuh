@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace ftb {
 
@@ -54,6 +55,54 @@ __device__ __forceinline__ cplx ldgc(const cplx* p) {
 __host__ __device__ inline cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
 __host__ __device__ inline cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every kernel of the fast-solve schedule is launched with programmatic stream
+// serialization: it lets the next kernel's CTAs launch as soon as all CTAs of
+// the running one have started, so launch latency and prologues overlap the
+// predecessor's tail.  Each such kernel calls pdl_wait() before its first
+// access to data another kernel of the solve writes or reads (every CTA calls
+// it, so completion of kernel k implies completion of k-1: transitive).
+__device__ __forceinline__ void pdl_launch_dependents(int on) {
+    if (on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// FT_PDL: unset/0 = off (measured: with an early trigger cfg4 went 420 -> 473 ms),
+// 1 = trigger at kernel start, 2 = implicit trigger at CTA exit (launch latency only)
+inline int pdl_mode() {
+    static const int m = getenv("FT_PDL") ? atoi(getenv("FT_PDL")) : 0;
+    return m;
+}
+inline bool pdl_enabled() { return pdl_mode() != 0; }
+
+// cudaLaunchKernelEx with PDL (when enabled) and an optional cluster size
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             unsigned cluster, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ---- launch arguments ------------------------------------------------------
 
 struct LeafArgs {
@@ -84,6 +133,7 @@ struct LeafArgs {
     unsigned* bar;             // fused slab leaf: grid-barrier counter (zeroed per solve)
     unsigned bar_target;       // value the counter reaches when every CTA of this leaf arrived
     long long* dbg_clk;        // diagnostics: per-phase clock64 stamps of CTA 0 (null = off)
+    int pdl_trigger;           // PDL: signal dependents at kernel start (pdl_mode() == 1)
     double* V;                 // Scheme 2 (single slab): V = U_i + U_(i-1) written next to U, else null
     int stencil;               // Scheme 2: in-leaf history acts on U_i + U_(i-1)
 };
@@ -104,6 +154,7 @@ struct MpArgs {
     int J;                     // near-field lags summed exactly: 1..J-1
     cplx* scratch;             // split K-branch levels: branch results [pairs][K][m]
     int pair_begin, pair_count;  // split K-branch levels: pairs of this launch
+    int pdl_trigger;           // PDL: signal dependents at kernel start (pdl_mode() == 1)
 };
 
 struct DirectArgs {

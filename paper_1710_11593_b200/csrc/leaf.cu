@@ -241,6 +241,9 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     (void)colp;
 
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    ScanConsts<NPT> sc;
+    scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);  // plan constants: before the dependency wait
+    pdl_wait();
     if (stamp) a.dbg_clk[8] = clock64();
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
@@ -255,8 +258,6 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? s_out[q * (L + 1) + k] : 0.0;
     }
     __syncthreads();
-    ScanConsts<NPT> sc;
-    scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);
     if (stamp) a.dbg_clk[9] = clock64();
     // Dirichlet correction coefficients (SINGLE mode)
     double kF[NPT], kB[NPT];
@@ -351,6 +352,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 
 template <int KIND, int NPT, int L, int MODE>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
     extern __shared__ __align__(16) double s_dyn0[];
     leaf_body<KIND, NPT, L, MODE>(a, s_dyn0, true);
 }
@@ -654,6 +656,8 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
 
 template <int KIND, int NPT, int L>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     extern __shared__ __align__(16) double s_dyn[];
     correct_body<KIND, NPT, L>(a, s_dyn, s_dyn + (uint64_t)L * (2 * a.P + 1), false);
 }
@@ -692,11 +696,10 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
         oattr = true;
     }
     if (!multi) {
-        leaf_kernel<KIND, NPT, L, 0><<<ctas, KIND == SK_DIAG ? threads : kLeafThreads, osmem, st>>>(a);
-        return cudaGetLastError();
+        return launch_ex(leaf_kernel<KIND, NPT, L, 0>, dim3(ctas), dim3(KIND == SK_DIAG ? threads : kLeafThreads), osmem,
+                         st, 1, a);
     }
-    leaf_kernel<KIND, NPT, L, 1><<<ctas, kLeafThreads, osmem, st>>>(a);
-    return cudaGetLastError();
+    return launch_ex(leaf_kernel<KIND, NPT, L, 1>, dim3(ctas), dim3(kLeafThreads), osmem, st, 1, a);
 }
 
 template <int KIND, int NPT, int L>
@@ -708,8 +711,7 @@ static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
-    leaf_correct<KIND, NPT, L><<<ctas, kLeafThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_ex(leaf_correct<KIND, NPT, L>, dim3(ctas), dim3(kLeafThreads), smem, st, 1, a);
 }
 
 template <int KIND, int NPT, int L>

@@ -68,6 +68,8 @@ __device__ __forceinline__ void mid_inv(cplx* buf, int total, const cplx* tw) {
 // cluster barriers, ncu).
 template <int K, int LOGM, bool SPLIT, bool FOLDED = false>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* buf = reinterpret_cast<cplx*>(smem_raw);
     __shared__ PairInfo s_pair[kMpTile / 32];
@@ -269,6 +271,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
 // per point, ncu).
 template <int K, int LOGM>
 __global__ void __launch_bounds__(kMpThreads) mp_fold_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     constexpr int m = 1 << LOGM;
     const int n = a.n;
     const int pl = blockIdx.y;
@@ -302,6 +306,8 @@ __global__ void __launch_bounds__(kMpThreads) mp_fold_kernel(MpArgs a) {
 // target outputs t = mid + (q - K/2) m + r (plus the exact near field).
 template <int K, int LOGM>
 __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     constexpr int m = 1 << LOGM;
     const int n = a.n;
     const int pl = blockIdx.y;  // pair within the batch
@@ -458,6 +464,8 @@ template <int LOGN>
 #define FT_MP1_MINB 2
 #endif
 __global__ void __launch_bounds__(kMpThreads, FT_MP1_MINB) mp1_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     using PL = Plan1<LOGN>;
     constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
     constexpr int G = n >= kMpTile ? 1 : kMpTile / n;
@@ -610,6 +618,8 @@ __device__ __forceinline__ void mid_inv_g(cplx* buf, int total, const cplx* tw, 
 
 template <int LOGN>
 __global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     using PL = Plan1<LOGN>;
     constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
     static_assert(n <= kMpTile, "group-private plan needs n <= kMpTile");
@@ -774,6 +784,8 @@ __global__ void __launch_bounds__(kMpThreads, 1) spec1_kernel(const double* col,
 // broadcast), and the 16x16 block products are fully unrolled on registers.
 template <int H>
 __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
     constexpr int TT = H < 16 ? H : 16;
     constexpr int TPR = H / TT;                      // threads per row
     constexpr int RPC = kMpThreads / TPR;            // rows per CTA
@@ -935,15 +947,20 @@ static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
         a.pair_begin = p0;
         a.pair_count = std::min(batch, npairs - p0);
         if (prefold) {
-            mp_fold_kernel<K, LOGM><<<dim3(m / kMpThreads, a.pair_count), kMpThreads, 0, st>>>(a);
-            mp_kernel<K, LOGM, true, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+            cudaError_t e = launch_ex(mp_fold_kernel<K, LOGM>, dim3(m / kMpThreads, a.pair_count), dim3(kMpThreads),
+                                      0, st, 1, a);
+            if (e != cudaSuccess) return e;
+            e = launch_ex(mp_kernel<K, LOGM, true, true>, dim3(K, a.pair_count), dim3(kMpThreads),
+                          mp_smem_bytes(a.G, m), st, 1, a);
+            if (e != cudaSuccess) return e;
         } else {
-            mp_kernel<K, LOGM, true><<<dim3(K, a.pair_count), kMpThreads, mp_smem_bytes(a.G, m), st>>>(a);
+            cudaError_t e = launch_ex(mp_kernel<K, LOGM, true>, dim3(K, a.pair_count), dim3(kMpThreads),
+                                      mp_smem_bytes(a.G, m), st, 1, a);
+            if (e != cudaSuccess) return e;
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        mpB_kernel<K, LOGM><<<dim3(m / kMpThreads, a.pair_count), kMpThreads, 0, st>>>(a);
-        e = cudaGetLastError();
+        e = launch_ex(mpB_kernel<K, LOGM>, dim3(m / kMpThreads, a.pair_count), dim3(kMpThreads), 0, st, 1, a);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -959,19 +976,8 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
         if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(K, groups, 1);
-    cfg.blockDim = dim3(kMpThreads, 1, 1);
-    cfg.dynamicSmemBytes = mp_smem_bytes(a.G, a.m);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = K;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mp_kernel<K, LOGM, false>, a);
+    return launch_ex(mp_kernel<K, LOGM, false>, dim3(K, groups, 1), dim3(kMpThreads), mp_smem_bytes(a.G, a.m), st,
+                     (unsigned)K, a);
 }
 
 template <int H>
@@ -984,8 +990,7 @@ static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
         attr_set = true;
     }
     const int ctas = (a.rows + RPC - 1) / RPC;
-    mp_direct_kernel<H><<<ctas, kMpThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_ex(mp_direct_kernel<H>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
 }
 
 bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
@@ -1017,12 +1022,10 @@ static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
                 cudaFuncSetAttribute(mp1g_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 gattr = true;
             }
-            mp1g_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
-            return cudaGetLastError();
+            return launch_ex(mp1g_kernel<LOGN>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
         }
     }
-    mp1_kernel<LOGN><<<ctas, kMpThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_ex(mp1_kernel<LOGN>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
 }
 
 template <int LOGN>
