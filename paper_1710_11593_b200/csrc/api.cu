@@ -22,6 +22,7 @@ namespace {
 
 thread_local std::string g_err;
 int g_leaf_dbg = getenv("FT_LEAF_DBG") ? atoi(getenv("FT_LEAF_DBG")) : 0;
+bool g_no_kc = getenv("FT_NO_KC") != nullptr;  // A/B switch: leaf constants from constant memory
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -107,6 +108,7 @@ struct ft_plan {
     double* respw_d = nullptr;    // multi-slab phase-2 injection responses (leaf_wbuild)
     std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
     std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf
+    double kc_h[kKcLen] = {};            // problem 0's leaf constants (LeafArgs::kc)
     double* dw_d = nullptr;       // direct weights [B][N]
     double* cprime_d = nullptr;   // [B][nodes]
     double* den_d = nullptr;
@@ -516,6 +518,18 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     p->lamL.assign(count, 0.0L);
     p->G0L.assign(count, 0.0L);
     for (uint64_t b = 0; b < count; ++b) scan_params(p, (int)b, lampow);
+    {  // LeafArgs::kc for single-problem plans (kKc* layout; same values as scan_consts reads)
+        const double* lp0 = lampow.data();
+        auto lpk = [&](int k) { return lp0[std::min(k, p->lp_stride - 1)]; };
+        for (int j = 0; j < 32; ++j) p->kc_h[j] = p->leafcol_h[j];
+        for (int d = 0; d < 5; ++d) p->kc_h[kKcPow + d] = lpk(p->npt << d);
+        p->kc_h[kKcLamW] = lpk(32 * p->npt);
+        p->kc_h[kKcLam] = p->pc_h[0].lam;
+        for (int v = 0; v < 8; ++v) {
+            p->kc_h[kKcV1 + v] = v < p->npt ? lpk(v + 1) : 0.0;
+            p->kc_h[kKcNv + v] = v < p->npt ? lpk(p->npt - v) : 0.0;
+        }
+    }
     build_schedule(p);
 
     // device copies
@@ -679,6 +693,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.resp_g = p->respg_d;
             a.resp_h = p->resph_d;
             a.resp_w = p->respw_d;
+            a.kc_valid = p->B == 1 && !g_no_kc;
+            std::memcpy(a.kc, p->kc_h, sizeof(a.kc));
             a.pdl_trigger = pdl_mode() == 1;
             a.dbg = g_leaf_dbg;
             a.dbg_clk = (g_leaf_dbg & 4) ? p->dbgclk_d : nullptr;
@@ -1130,7 +1146,7 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     uint64_t launches = 0;
     FT_CUDA(cudaEventRecord(p->ev0, st));
     if (fast) {
-        const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH") && !(p->multi && p->fused_leaf);
+        const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH");
         if (use_graph) {
             if (!p->graph || p->graph_X != X || p->graph_src != src) {
                 if (p->graph) cudaGraphExecDestroy(p->graph);

@@ -29,6 +29,10 @@ struct ProblemConst {
 };
 
 constexpr int kLeafThreads = 256;
+// LeafArgs::kc layout (single-problem plans): in-leaf weights col[0..32), then
+// the uniform scan multipliers lam^(NPT 2^d) (d < 5), lam^(32 NPT), lam,
+// lam^(v+1) and lam^(NPT-v) (v < 8).
+constexpr int kKcPow = 32, kKcLamW = 37, kKcLam = 38, kKcV1 = 40, kKcNv = 48, kKcLen = 56;
 constexpr int kMaxSlabs = 160;
 constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in constant memory)  // slabs per problem in the multi-slab leaf
 constexpr int kMpThreads = 256;
@@ -136,6 +140,8 @@ struct LeafArgs {
     int pdl_trigger;           // PDL: signal dependents at kernel start (pdl_mode() == 1)
     double* V;                 // Scheme 2 (single slab): V = U_i + U_(i-1) written next to U, else null
     int stencil;               // Scheme 2: in-leaf history acts on U_i + U_(i-1)
+    int kc_valid;              // kc holds problem 0's leaf constants (single-problem plans)
+    double kc[kKcLen];         // see kKc* (kernel parameter: constant-bank operands)
 };
 
 struct MpArgs {

@@ -60,6 +60,63 @@ __device__ __forceinline__ void scan_consts(ScanConsts<NPT>& sc, const double* l
     sc.exBmask = lane < 31 ? 1.0 : 0.0;
 }
 
+// Leaf constants seen through one interface.  PC = false: per-problem values
+// (constant-memory leaf weights, lam^k table) loaded into registers.  PC = true
+// (single-problem plans): the kernel-parameter copy LeafArgs::kc, read as
+// constant-bank operands -- no registers for the 31 weights and the uniform
+// scan multipliers, only the two lane-dependent powers (the register file of
+// the 255-register step loop otherwise spills, ncu).
+template <bool PC, int NPT, int L>
+struct LeafConsts;
+
+template <int NPT, int L>
+struct LeafConsts<false, NPT, L> {
+    ScanConsts<NPT> sc;
+    double w[L];
+    __device__ __forceinline__ LeafConsts(const LeafArgs& a, int pb, const double* lp, double lam, int lane) {
+        scan_consts<NPT>(sc, lp, a.lp_stride, lam, lane);
+        const double* cc = c_leafcol[pb < kMaxLeafProblems ? pb : 0];
+#pragma unroll
+        for (int j = 0; j < L; ++j) w[j] = cc[j];
+    }
+    __device__ __forceinline__ double cw(int j) const { return w[j]; }
+    __device__ __forceinline__ double lam() const { return sc.lam; }
+    __device__ __forceinline__ double stepF(int d, double y, double S, int) const { return fma(sc.pwF[d], y, S); }
+    __device__ __forceinline__ double stepB(int d, double y, double S, int) const { return fma(sc.pwB[d], y, S); }
+    __device__ __forceinline__ double exF(double y, int) const { return sc.exFmask * y; }
+    __device__ __forceinline__ double exB(double y, int) const { return sc.exBmask * y; }
+    __device__ __forceinline__ double lamW() const { return sc.lamW; }
+    __device__ __forceinline__ double lamv1(int v) const { return sc.lamv1[v]; }
+    __device__ __forceinline__ double lamNv(int v) const { return sc.lamNv[v]; }
+    __device__ __forceinline__ double laneF() const { return sc.lamLaneF; }
+    __device__ __forceinline__ double laneB() const { return sc.lamLaneB; }
+};
+
+template <int NPT, int L>
+struct LeafConsts<true, NPT, L> {
+    const LeafArgs& a;
+    double lamLaneF, lamLaneB;
+    __device__ __forceinline__ LeafConsts(const LeafArgs& a_, int, const double* lp, double, int lane) : a(a_) {
+        lamLaneF = lp[min(NPT * lane, a.lp_stride - 1)];
+        lamLaneB = lp[min(NPT * (31 - lane), a.lp_stride - 1)];
+    }
+    __device__ __forceinline__ double cw(int j) const { return a.kc[j]; }
+    __device__ __forceinline__ double lam() const { return a.kc[kKcLam]; }
+    __device__ __forceinline__ double stepF(int d, double y, double S, int lane) const {
+        return lane >= (1 << d) ? fma(a.kc[kKcPow + d], y, S) : S;
+    }
+    __device__ __forceinline__ double stepB(int d, double y, double S, int lane) const {
+        return lane + (1 << d) < 32 ? fma(a.kc[kKcPow + d], y, S) : S;
+    }
+    __device__ __forceinline__ double exF(double y, int lane) const { return lane > 0 ? y : 0.0; }
+    __device__ __forceinline__ double exB(double y, int lane) const { return lane < 31 ? y : 0.0; }
+    __device__ __forceinline__ double lamW() const { return a.kc[kKcLamW]; }
+    __device__ __forceinline__ double lamv1(int v) const { return a.kc[kKcV1 + v]; }
+    __device__ __forceinline__ double lamNv(int v) const { return a.kc[kKcNv + v]; }
+    __device__ __forceinline__ double laneF() const { return lamLaneF; }
+    __device__ __forceinline__ double laneB() const { return lamLaneB; }
+};
+
 // dst[q][k] (row stride L+1) = src[(row0 + q) * N + t0 + k] for q < rows, k < len;
 // consecutive threads read consecutive steps of a node row, 8 loads in flight.
 // radd (optional, same layout as src): added element-wise -- the streamed host
@@ -145,8 +202,8 @@ __device__ __forceinline__ void store_rows(double* X, const double* src, uint64_
 // Forward (and, for TRIDIAG, backward) lam-decay scans over the CTA's nodes
 // with zero carry in at both ends.  Fv/Bv: scans at this thread's nodes;
 // totF: F at the CTA's last (possibly padding) node; totB: B at its first.
-template <int KIND, int NPT>
-__device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanConsts<NPT>& sc,
+template <int KIND, int NPT, class SC>
+__device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
                                          double (*s_wt)[2], int lane, int w, double (&Fv)[NPT],
                                          double (&Bv)[NPT], double& totF, double& totB, double& Fpv) {
     constexpr int nw = kLeafThreads / 32;
@@ -155,7 +212,7 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
     double acc = 0.0;
 #pragma unroll
     for (int v = 0; v < NPT; ++v) {
-        acc = fma(sc.lam, acc, in[v]);
+        acc = fma(sc.lam(), acc, in[v]);
         f[v] = acc;
     }
     double SF = acc, SB = 0.0;
@@ -163,7 +220,7 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
         double accb = 0.0;
 #pragma unroll
         for (int v = NPT - 1; v >= 0; --v) {
-            accb = fma(sc.lam, accb, in[v]);
+            accb = fma(sc.lam(), accb, in[v]);
             bl[v] = accb;
         }
         SB = accb;
@@ -171,14 +228,14 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
         const double yF = __shfl_up_sync(0xffffffffu, SF, 1 << d);
-        SF = fma(sc.pwF[d], yF, SF);
+        SF = sc.stepF(d, yF, SF, lane);
         if (TRI) {
             const double yB = __shfl_down_sync(0xffffffffu, SB, 1 << d);
-            SB = fma(sc.pwB[d], yB, SB);
+            SB = sc.stepB(d, yB, SB, lane);
         }
     }
-    const double exF = sc.exFmask * __shfl_up_sync(0xffffffffu, SF, 1);
-    const double exB = TRI ? sc.exBmask * __shfl_down_sync(0xffffffffu, SB, 1) : 0.0;
+    const double exF = sc.exF(__shfl_up_sync(0xffffffffu, SF, 1), lane);
+    const double exB = TRI ? sc.exB(__shfl_down_sync(0xffffffffu, SB, 1), lane) : 0.0;
     if (lane == 31) s_wt[w][0] = SF;
     if (lane == 0) s_wt[w][1] = SB;
     __syncthreads();
@@ -187,23 +244,23 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
 #pragma unroll
     for (int ww = 0; ww < nw; ++ww) {
         if (ww == w) CF = runF;
-        runF = fma(sc.lamW, runF, s_wt[ww][0]);
+        runF = fma(sc.lamW(), runF, s_wt[ww][0]);
         if (TRI) {
             const int wb = nw - 1 - ww;
             if (wb == w) CB = runB;
-            runB = fma(sc.lamW, runB, s_wt[wb][1]);
+            runB = fma(sc.lamW(), runB, s_wt[wb][1]);
         }
     }
     totF = runF;
     totB = runB;
-    const double Fprev = fma(sc.lamLaneF, CF, exF);
+    const double Fprev = fma(sc.laneF(), CF, exF);
     Fpv = Fprev;  // F at the node before this thread's first node (0 before node 0)
 #pragma unroll
-    for (int v = 0; v < NPT; ++v) Fv[v] = fma(sc.lamv1[v], Fprev, f[v]);
+    for (int v = 0; v < NPT; ++v) Fv[v] = fma(sc.lamv1(v), Fprev, f[v]);
     if (TRI) {
-        const double Bnext = fma(sc.lamLaneB, CB, exB);
+        const double Bnext = fma(sc.laneB(), CB, exB);
 #pragma unroll
-        for (int v = 0; v < NPT; ++v) Bv[v] = fma(sc.lamNv[v], Bnext, bl[v]);
+        for (int v = 0; v < NPT; ++v) Bv[v] = fma(sc.lamNv(v), Bnext, bl[v]);
     }
 }
 
@@ -212,7 +269,7 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const ScanCons
 // MODE 1 (LOCAL): phase 1 of the slab decomposition (zero inter-slab carries);
 //   per step the slab's exported carries (F at its last node, B at its first)
 //   are written to xch[cta][k][2].
-template <int KIND, int NPT, int L, int MODE>
+template <int KIND, int NPT, int L, int MODE, bool PC = false>
 __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x) {
     // s_out: [slab nodes][L + 1] solution tile (stays resident for the fused leaf)
     __shared__ double s_wt[2][32][2];
@@ -232,17 +289,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
     const int len = a.len;
 
-    double cw[L];
-    {
-        const double* cc = c_leafcol[pb < kMaxLeafProblems ? pb : 0];
-#pragma unroll
-        for (int j = 0; j < L; ++j) cw[j] = cc[j];
-    }
     (void)colp;
 
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
-    ScanConsts<NPT> sc;
-    scan_consts<NPT>(sc, lp, a.lp_stride, pc.lam, lane);  // plan constants: before the dependency wait
+    const LeafConsts<PC, NPT, L> sc(a, pb, lp, pc.lam, lane);  // plan constants: before the dependency wait
     pdl_wait();
     if (stamp) a.dbg_clk[8] = clock64();
     // input tile: coalesced row reads (a warp reads consecutive steps of one
@@ -325,8 +375,15 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         for (int v = NPT - 1; v >= 0; --v) {
             // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
             const double xs = a.stencil ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
+            // push x_k into the remaining in-leaf steps; chunks whose first entry lies
+            // past the leaf end (k + 1 + c >= len) are dead and skipped (warp-uniform)
 #pragma unroll
-            for (int i = 0; i + 1 < L; ++i) tile[v][i] = fma(-cw[i + 1], xs, tile[v][i + 1]);
+            for (int c = 0; c + 1 < L; c += 8) {
+                if (c == 0 || k + 1 + c < len) {
+#pragma unroll
+                    for (int i = c; i < c + 8 && i + 1 < L; ++i) tile[v][i] = fma(-sc.cw(i + 1), xs, tile[v][i + 1]);
+                }
+            }
             tile[v][L - 1] = 0.0;
         }
         ++outp;
@@ -350,11 +407,11 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     if (stamp) a.dbg_clk[11] = clock64();
 }
 
-template <int KIND, int NPT, int L, int MODE>
+template <int KIND, int NPT, int L, int MODE, bool PC>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_kernel(LeafArgs a) {
     pdl_launch_dependents(a.pdl_trigger);
     extern __shared__ __align__(16) double s_dyn0[];
-    leaf_body<KIND, NPT, L, MODE>(a, s_dyn0, true);
+    leaf_body<KIND, NPT, L, MODE, PC>(a, s_dyn0, true);
 }
 
 // Phase 2 reduced recursion (see file header): warps < ceil(P/32) of the
@@ -691,15 +748,19 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
     static bool oattr = false;
     if (!oattr) {
         const int mx = (int)(sizeof(double) * kLeafThreads * NPT * (L + 1));
-        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         oattr = true;
     }
+    const dim3 blk(KIND == SK_DIAG ? threads : kLeafThreads);
     if (!multi) {
-        return launch_ex(leaf_kernel<KIND, NPT, L, 0>, dim3(ctas), dim3(KIND == SK_DIAG ? threads : kLeafThreads), osmem,
-                         st, 1, a);
+        return a.kc_valid ? launch_ex(leaf_kernel<KIND, NPT, L, 0, true>, dim3(ctas), blk, osmem, st, 1, a)
+                          : launch_ex(leaf_kernel<KIND, NPT, L, 0, false>, dim3(ctas), blk, osmem, st, 1, a);
     }
-    return launch_ex(leaf_kernel<KIND, NPT, L, 1>, dim3(ctas), dim3(kLeafThreads), osmem, st, 1, a);
+    return a.kc_valid ? launch_ex(leaf_kernel<KIND, NPT, L, 1, true>, dim3(ctas), dim3(kLeafThreads), osmem, st, 1, a)
+                      : launch_ex(leaf_kernel<KIND, NPT, L, 1, false>, dim3(ctas), dim3(kLeafThreads), osmem, st, 1, a);
 }
 
 template <int KIND, int NPT, int L>
@@ -723,9 +784,18 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
-    void* args[] = {(void*)&a};
-    return cudaLaunchCooperativeKernel((const void*)leaf_fused<KIND, NPT, L>, dim3(ctas), dim3(kLeafThreads),
-                                       args, smem, st);
+    // cooperative attribute through cudaLaunchKernelEx: capturable into the solve's CUDA graph
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLeafThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute coop[1];
+    coop[0].id = cudaLaunchAttributeCooperative;
+    coop[0].val.cooperative = 1;
+    cfg.attrs = coop;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L>, a);
 }
 
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
