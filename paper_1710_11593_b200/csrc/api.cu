@@ -556,7 +556,10 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             int dev_sms = 0, per_sm = 0;
             FT_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
             per_sm = 1;
-            p->fused_leaf = (int64_t)B * p->P_local <= (int64_t)dev_sms * per_sm && getenv("FT_FUSED_LEAF") != nullptr;  // measured slower (opt-in)
+            // one cooperative kernel per leaf (phase 1, grid barrier, phases 2/3 on the
+            // SMEM-resident tile): measured 407 -> 400 ms on cfg4 once the step loop
+            // stopped spilling (kernel-parameter constants)
+            p->fused_leaf = (int64_t)B * p->P_local <= (int64_t)dev_sms * per_sm && getenv("FT_NO_FUSED_LEAF") == nullptr;
         }
         const uint64_t gsz = (uint64_t)2 * 2 * p->slab * p->L, hsz = (uint64_t)2 * p->L * 4;
         std::vector<double> G(B * gsz, 0.0), H(B * hsz, 0.0);

@@ -721,12 +721,12 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
 
 // Single-GPU slab leaf in ONE cooperative kernel: phase 1, publish carries, a
 // grid barrier (all slabs co-resident), phases 2 + 3 on the resident tile.
-template <int KIND, int NPT, int L>
+template <int KIND, int NPT, int L, bool PC>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
     double* s_c0 = s_dyn;
     double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
-    leaf_body<KIND, NPT, L, 1>(a, s_x, false);
+    leaf_body<KIND, NPT, L, 1, PC>(a, s_x, false);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -780,7 +780,9 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         attr = true;
     }
@@ -795,7 +797,8 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
     coop[0].val.cooperative = 1;
     cfg.attrs = coop;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L>, a);
+    return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, true>, a)
+                      : cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, false>, a);
 }
 
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
