@@ -307,6 +307,24 @@ def run_ours(args, world, rank, local):
         lv["ms"] += o["ms"]
         lv["bytes"] += o["bytes"]
 
+    # the same solve with the separable forcing generated inside the leaves
+    # (ft_solve_fast_modes: no RHS array, no RHS read -- SURVEY.md 8f item 2)
+    fused = None
+    if not sharded and plan.B == wl.B and not args.no_fused:
+        plan.solve_fast_modes(u, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            f0.record(stream)
+            for _ in range(args.steps):
+                plan.solve_fast_modes(u, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
+            f1.record(stream)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / args.steps
+        fused = {"value": total_unknowns / (fms / 1e3), "unit": "unknowns/s", "ms_per_step": fms,
+                 "path": "ft_solve_fast_modes (RHS generated in the leaves; includes the per-call table setup)"}
+
     e2e = None
     if not args.no_e2e:
         h_rhs = torch.empty(shape, dtype=torch.float64, pin_memory=True)
@@ -358,6 +376,7 @@ def run_ours(args, world, rank, local):
                               "leaf_gbs": lf_bytes / (lf_ms / 1e3) / 1e9 if lf_ms else None,
                               "mp_levels": per_level},
             "e2e": e2e,
+            "fused_rhs": fused,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_solve * args.steps,
             "clocks": clk.summary(),
@@ -377,6 +396,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fused", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

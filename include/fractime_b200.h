@@ -173,6 +173,14 @@ int ft_assemble_rhs_modes(const ft_plan* plan, int nmodes, const double* a, cons
                           const double* phi_amp, double* rhs_device);
 
 int ft_solve_fast(ft_plan* plan, const double* rhs, double* u, ft_report* report);
+/* Fast solve with the separable forcing of ft_assemble_rhs_modes generated
+ * inside the leaf kernels: the right-hand side is never
+ * materialised (no RHS array, no RHS read); the history products accumulate
+ * from zero and each leaf adds sum_j A[node][j] T[step][j] while staging.  u:
+ * host or device, [rows][N].  Same arguments as ft_assemble_rhs_modes. */
+int ft_solve_fast_modes(ft_plan* plan, int nmodes, const double* a, const double* k, const double* p,
+                        const int* trig, const double* u0_amp, const double* phi_amp, double* u,
+                        ft_report* report);
 int ft_solve_direct(ft_plan* plan, const double* rhs, double* u, ft_report* report);
 
 /* Diagnostics: one fast solve (device buffers only) with a CUDA event

@@ -94,6 +94,7 @@ _lib = None
 
 ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exchange", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
+               "ft_solve_fast_modes",
                "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy",
                "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec")
 
@@ -120,6 +121,7 @@ def lib() -> C.CDLL:
         L.ft_assemble_rhs_modes.argtypes = [P, I, P, P, P, P, P, P, P]
         L.ft_solve_fast.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
+        L.ft_solve_fast_modes.argtypes = [P, I, P, P, P, P, P, P, P, C.POINTER(_Report)]
         L.ft_set_stream.argtypes = [P, P]
         L.ft_profile_fast.argtypes = [P, P, P, C.POINTER(_OpTime), U64, C.POINTER(U64)]
         L.ft_schedule.argtypes = [U64, U64, C.POINTER(_OpTime), U64, C.POINTER(U64)]
@@ -328,6 +330,23 @@ class Plan:
 
     def solve_direct(self, rhs, out=None):
         return self._solve(lib().ft_solve_direct, rhs, out)
+
+    def solve_fast_modes(self, out, a, k, p, trig, u0amp=None, phiamp=None):
+        """Fast solve with the separable forcing of assemble_rhs_modes generated
+        inside the leaves (the right-hand side is never materialised); `out`
+        (host or device, [rows][N]) receives U."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        trig = np.ascontiguousarray(trig, dtype=np.int32)
+        u0amp = None if u0amp is None else np.ascontiguousarray(u0amp, dtype=np.float64)
+        phiamp = None if phiamp is None else np.ascontiguousarray(phiamp, dtype=np.float64)
+        rep = _Report()
+        _check(lib().ft_solve_fast_modes(self._h, len(k), a.ctypes.data, k.ctypes.data, p.ctypes.data,
+                                         trig.ctypes.data, None if u0amp is None else u0amp.ctypes.data,
+                                         None if phiamp is None else phiamp.ctypes.data, _ptr(out), C.byref(rep)))
+        return out, SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
+                                rep.device_ms, rep.kernel_launches)
 
 
 def schedule(time_steps: int, leaf: int = 32):

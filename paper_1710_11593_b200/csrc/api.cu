@@ -121,6 +121,12 @@ struct ft_plan {
     cudaGraphExec_t graph = nullptr;
     const void* graph_X = nullptr;
     const void* graph_src = nullptr;
+    const void* graph_gen = nullptr;
+    double* genA_d = nullptr;     // ft_solve_fast_modes tables
+    double* genT_d = nullptr;
+    size_t genA_bytes = 0, genT_bytes = 0;
+    double* genArgs_d = nullptr;  // ft_solve_fast_modes argument block
+    size_t genArgs_bytes = 0;
     uint64_t graph_launches = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -638,6 +644,12 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
 // products accumulate into a zeroed X, linear in R); finished chunks of U
 // leave on a second copy stream as soon as their last leaf is done.  PCIe
 // traffic in both directions overlaps the solve.
+struct GenRhs {                   // fused separable RHS (ft_solve_fast_modes)
+    const double* A = nullptr;
+    const double* T = nullptr;
+    int J = 0;
+};
+
 struct StreamIO {
     uint64_t C = 0;               // chunk steps (multiple of the leaf length)
     bool defer = false;           // R streamed into rdev (leaves add it)
@@ -647,7 +659,7 @@ struct StreamIO {
 };
 
 int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
-             std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr) {
+             std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr, const GenRhs* gen = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
     // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve;
@@ -669,6 +681,10 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             const bool defer = io && io->defer;
             a.src = (op.first && !defer) ? rhs : X;
             a.radd = defer ? io->rdev : nullptr;
+            a.genA = gen ? gen->A : nullptr;
+            a.genT = gen ? gen->T : nullptr;
+            a.genJ = gen ? gen->J : 0;
+            if (gen && op.first) a.src = nullptr;  // nothing accumulated in X yet: history starts at zero
             if (defer) {  // this leaf's R chunk must have landed
                 const uint64_t c = op.t0 / io->C;
                 if (c >= io->waited) {
@@ -736,6 +752,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.U = p->stencil ? p->vsrc_d : X;
             a.pdl_trigger = pdl_mode() == 1;
             a.rsrc = (op.first && !(io && io->defer)) ? rhs : X;
+            if (gen && op.first) a.rsrc = nullptr;  // first touch of these targets: the history starts at zero
             a.N = N;
             a.lo = op.t0;
             a.mid = op.mid;
@@ -1113,6 +1130,41 @@ static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* r
     return FT_OK;
 }
 
+// One fast solve on the plan's stream: replayed as a CUDA graph (single
+// rank; keyed by the buffers and the fused-RHS tables), else launched directly.
+static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* gen, uint64_t* launches) {
+    const cudaStream_t st = p->stream;
+    const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH");
+    if (!use_graph) return run_fast(p, X, src, launches, nullptr, nullptr, gen);
+    const void* gkey = gen ? (const void*)gen->A : nullptr;
+    if (!p->graph || p->graph_X != X || p->graph_src != src || p->graph_gen != gkey) {
+        if (p->graph) cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+        cudaStream_t cs;
+        FT_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        FT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        const cudaStream_t keep = p->stream;
+        p->stream = cs;
+        int rc = run_fast(p, X, src, &p->graph_launches, nullptr, nullptr, gen);
+        p->stream = keep;
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        FT_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+        cudaGraphDestroy(g);
+        FT_CUDA(ie);
+        p->graph_X = X;
+        p->graph_src = src;
+        p->graph_gen = gkey;
+    }
+    FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
+    FT_CUDA(cudaGraphLaunch(p->graph, st));
+    *launches = p->graph_launches;
+    return FT_OK;
+}
+
 static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool fast) {
     if (!p || !rhs || !u) return set_err(FT_EINVAL, "ft_solve: null argument");
     if (!fast && p->part_world > 1) return set_err(FT_EINVAL, "ft_solve_direct: not available on partitioned plans");
@@ -1149,36 +1201,8 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     uint64_t launches = 0;
     FT_CUDA(cudaEventRecord(p->ev0, st));
     if (fast) {
-        const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH");
-        if (use_graph) {
-            if (!p->graph || p->graph_X != X || p->graph_src != src) {
-                if (p->graph) cudaGraphExecDestroy(p->graph);
-                p->graph = nullptr;
-                cudaStream_t cs;
-                FT_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-                FT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-                const cudaStream_t keep = p->stream;
-                p->stream = cs;
-                int rc = run_fast(p, X, src, &p->graph_launches);
-                p->stream = keep;
-                cudaGraph_t g = nullptr;
-                const cudaError_t ce = cudaStreamEndCapture(cs, &g);
-                cudaStreamDestroy(cs);
-                if (rc) return rc;
-                FT_CUDA(ce);
-                const cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
-                cudaGraphDestroy(g);
-                FT_CUDA(ie);
-                p->graph_X = X;
-                p->graph_src = src;
-            }
-            FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
-            FT_CUDA(cudaGraphLaunch(p->graph, st));
-            launches = p->graph_launches;
-        } else {
-            int rc = run_fast(p, X, src, &launches);
-            if (rc) return rc;
-        }
+        int rc = launch_fast(p, X, src, nullptr, &launches);
+        if (rc) return rc;
     } else {
         if (src != X) FT_CUDA(cudaMemcpyAsync(X, src, bytes, cudaMemcpyDeviceToDevice, st));
         DirectArgs da;
@@ -1219,6 +1243,120 @@ int ft_solve_fast(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
 
 int ft_solve_direct(ft_plan* p, const double* rhs, double* u, ft_report* rep) {
     return solve_common(p, rhs, u, rep, false);
+}
+
+// Fast solve with the separable forcing generated inside the leaves (SURVEY 8f
+// item 2): R is never materialised -- the history products accumulate into X
+// from zero and each leaf adds sum_j A[row][j] T[n][j] while staging its tile.
+int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k, const double* pe,
+                        const int* trig, const double* u0amp, const double* phiamp, double* u, ft_report* rep) {
+    if (p && p->custom) return set_err(FT_EINVAL, "ft_solve_fast_modes: plan from ft_setup_toeplitz has no scheme");
+    if (!p || !u || nmodes < 0 || (nmodes && (!a || !k || !pe || !trig)))
+        return set_err(FT_EINVAL, "ft_solve_fast_modes: bad argument");
+    const auto t_start = std::chrono::steady_clock::now();
+    FT_CUDA(cudaSetDevice(p->device));
+    const cudaStream_t st = p->stream;
+    const int B = p->B;
+    // small argument arrays in one plan-owned device block (no per-call cudaMalloc)
+    const size_t nm = (size_t)std::max(1, nmodes);
+    std::vector<double> hb;
+    hb.reserve(2 * B * nm + nm + 3 * B + nm);
+    auto put = [&](const double* x, size_t n) {
+        const size_t off = hb.size();
+        for (size_t i = 0; i < n; ++i) hb.push_back(x ? x[i] : 0.0);
+        return off;
+    };
+    const size_t oa = put(nmodes ? a : nullptr, B * nm), ok = put(nmodes ? k : nullptr, nm),
+                 op = put(nmodes ? pe : nullptr, B * nm);
+    std::vector<double> cv(B);
+    for (int b = 0; b < B; ++b) cv[b] = p->c[b];
+    const size_t oc = put(cv.data(), B), ou = put(u0amp, B), of = put(phiamp, B);
+    const size_t ot = hb.size();
+    hb.resize(hb.size() + (nm + 1) / 2, 0.0);  // trig ids: nm contiguous ints in the tail
+    {
+        std::vector<int> tv(nm, 2);
+        for (size_t i = 0; i < (size_t)nmodes; ++i) tv[i] = trig[i];
+        std::memcpy(hb.data() + ot, tv.data(), sizeof(int) * nm);
+    }
+    int rc;
+    if (hb.size() * sizeof(double) > p->genArgs_bytes) {
+        if (p->genArgs_d) cudaFree(p->genArgs_d);
+        p->genArgs_d = nullptr;
+        if ((rc = alloc_copy((void**)&p->genArgs_d, nullptr, hb.size() * sizeof(double)))) return rc;
+        p->genArgs_bytes = hb.size() * sizeof(double);
+    }
+    FT_CUDA(cudaMemcpyAsync(p->genArgs_d, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    const double* gd = p->genArgs_d;
+    const double *a_d = gd + oa, *k_d = gd + ok, *p_d = gd + op, *c_d = gd + oc;
+    const double* u_d = u0amp ? gd + ou : nullptr;
+    const double* f_d = phiamp ? gd + of : nullptr;
+    const int* t_d = reinterpret_cast<const int*>(gd + ot);
+    RhsModesArgs ra;
+    ra.R = nullptr;
+    ra.N = p->N;
+    ra.nodes = p->local_nodes;
+    ra.B = B;
+    ra.nmodes = nmodes;
+    ra.scheme = p->scheme;
+    ra.rhs_mode = p->rhs_mode;
+    ra.node_begin = p->node_begin;
+    ra.h = p->h;
+    ra.tau = p->tau;
+    ra.a = a_d;
+    ra.k = k_d;
+    ra.p = p_d;
+    ra.trig = t_d;
+    ra.u0amp = u_d;
+    ra.phiamp = f_d;
+    ra.wts = p->wts_d;
+    ra.cvals = c_d;
+    const int J = std::max(1, gen_terms(ra));
+    const size_t ab = sizeof(double) * rows_of(p) * J, tb = sizeof(double) * (size_t)B * p->N * J;
+    if (ab != p->genA_bytes) {
+        if (p->genA_d) cudaFree(p->genA_d);
+        p->genA_d = nullptr;
+        if ((rc = alloc_copy((void**)&p->genA_d, nullptr, ab))) return rc;
+        p->genA_bytes = ab;
+    }
+    if (tb != p->genT_bytes) {
+        if (p->genT_d) cudaFree(p->genT_d);
+        p->genT_d = nullptr;
+        if ((rc = alloc_copy((void**)&p->genT_d, nullptr, tb))) return rc;
+        p->genT_bytes = tb;
+    }
+    if (gen_terms(ra) == 0) {  // homogeneous: all-zero tables
+        FT_CUDA(cudaMemsetAsync(p->genA_d, 0, ab, st));
+        FT_CUDA(cudaMemsetAsync(p->genT_d, 0, tb, st));
+    } else {
+        FT_CUDA(launch_gen_tables(ra, p->genA_d, p->genT_d, st));
+    }
+    GenRhs gen;
+    gen.A = p->genA_d;
+    gen.T = p->genT_d;
+    gen.J = J;
+    const bool u_dev = is_device_ptr(u);
+    double* X = u;
+    if (!u_dev) {
+        if ((rc = ensure_work(p))) return rc;
+        X = p->work_d;
+    }
+    uint64_t launches = 0;
+    FT_CUDA(cudaEventRecord(p->ev0, st));
+    if ((rc = launch_fast(p, X, nullptr, &gen, &launches))) return rc;
+    FT_CUDA(cudaEventRecord(p->ev1, st));
+    if (!u_dev) FT_CUDA(cudaMemcpyAsync(u, X, sizeof(double) * rows_of(p) * p->N, cudaMemcpyDeviceToHost, st));
+    FT_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    FT_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    if (rep) {
+        std::snprintf(rep->method, sizeof(rep->method), "%s", "fast");
+        rep->iterations = 0;
+        rep->residual = 0.0;
+        rep->device_ms = ms;
+        rep->kernel_launches = launches;
+        rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+    return FT_OK;
 }
 
 // diagnostics: the clock64 stamps of the last slab leaf (FT_LEAF_DBG & 4)
@@ -1303,7 +1441,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);

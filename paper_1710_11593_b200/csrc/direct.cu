@@ -134,6 +134,71 @@ __global__ void rhs_modes_kernel(RhsModesArgs a) {
     }
 }
 
+// Separable factors of the same right-hand side for the fused path
+// (ft_solve_fast_modes): R[row][n] = sum_j A[row][j] T[b][n][j], with the terms
+// in rhs_modes_kernel's order (modes, then phi (wave), then u0) and the same
+// rounded products, so the leaf's sum reproduces rhs_modes_kernel's value.
+int gen_terms(const RhsModesArgs& a) {
+    return a.nmodes + (a.scheme == 2 && a.phiamp ? 1 : 0) + (a.u0amp ? 1 : 0);
+}
+
+__global__ void gen_tables_kernel(RhsModesArgs a, double* A, double* T, int J) {
+    const double pi = 3.14159265358979323846;
+    const uint64_t rows = (uint64_t)a.B * a.nodes;
+    const uint64_t nA = rows, nT = (uint64_t)a.B * a.N;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < nA + nT;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        if (idx < nA) {  // node factors
+            const uint64_t row = idx;
+            const int pb = (int)(row / a.nodes);
+            const int i = a.node_begin + (int)(row % a.nodes) + 1;
+            const double x = a.scheme == 0 ? 0.0 : a.scheme == 1 ? ((double)i - 0.5) * a.h : (double)i * a.h;
+            double* Ar = A + row * J;
+            int j = 0;
+            for (; j < a.nmodes; ++j) {
+                const int tg = a.trig[j];
+                const double sp = tg == 0   ? sin(a.k[j] * pi * x)
+                                  : tg == 1 ? cos(a.k[j] * pi * x)
+                                  : tg == 3 ? x * (1.0 - x)
+                                  : tg == 4 ? (1.0 - 2.0 * x)
+                                            : 1.0;
+                Ar[j] = a.a[pb * a.nmodes + j] * sp;
+            }
+            const double xi = a.scheme == 0 ? 0.0 : (double)i * a.h;
+            if (a.scheme == 2 && a.phiamp) Ar[j++] = a.phiamp[pb] * sin(pi * xi);
+            if (a.u0amp) {
+                if (a.scheme == 1)
+                    Ar[j++] = a.u0amp[pb] * sin(pi * ((double)i * a.h)) + a.u0amp[pb] * sin(pi * ((double)(i - 1) * a.h));
+                else
+                    Ar[j++] = a.u0amp[pb] * (a.scheme == 0 ? 1.0 : sin(pi * xi));
+            }
+        } else {  // step factors
+            const uint64_t e = idx - nA;
+            const int pb = (int)(e / a.N);
+            const uint64_t n0 = e % a.N;
+            const double n = (double)(n0 + 1);
+            const double t = a.scheme == 2 ? (n - 0.5) * a.tau : n * a.tau;
+            const double* wv = a.wts + (uint64_t)pb * (a.N + 1);
+            const double c = a.cvals[pb];
+            double* Tr = T + e * J;
+            int j = 0;
+            for (; j < a.nmodes; ++j) Tr[j] = pow(t, a.p[pb * a.nmodes + j]);
+            if (a.scheme == 2) {
+                if (a.phiamp) Tr[j++] = c * a.tau * wv[n0];
+                if (a.u0amp)  // v -= c (M_(n-2) - M_(n-1)) u0 for n >= 2; corrected mode adds c M_0 u0 at n = 1
+                    Tr[j++] = n0 >= 1 ? -(c * (wv[n0 - 1] - wv[n0])) : (a.rhs_mode == 1 ? c * wv[0] : 0.0);
+            } else if (a.u0amp) {
+                Tr[j++] = c * wv[n0];
+            }
+        }
+    }
+}
+
+cudaError_t launch_gen_tables(const RhsModesArgs& a, double* A, double* T, cudaStream_t st) {
+    gen_tables_kernel<<<148 * 4, 256, 0, st>>>(a, A, T, gen_terms(a));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st) {
     rhs_modes_kernel<<<148 * 8, 256, 0, st>>>(a);
     return cudaGetLastError();

@@ -140,6 +140,9 @@ struct LeafArgs {
     int pdl_trigger;           // PDL: signal dependents at kernel start (pdl_mode() == 1)
     double* V;                 // Scheme 2 (single slab): V = U_i + U_(i-1) written next to U, else null
     int stencil;               // Scheme 2: in-leaf history acts on U_i + U_(i-1)
+    const double* genA;        // fused separable RHS (ft_solve_fast_modes): [rows][genJ] node factors
+    const double* genT;        //   [B][N][genJ] step factors; R = sum_j genA * genT added at staging
+    int genJ;                  //   (null genA: R comes from src)
     int kc_valid;              // kc holds problem 0's leaf constants (single-problem plans)
     double kc[kKcLen];         // see kKc* (kernel parameter: constant-bank operands)
 };
@@ -147,7 +150,7 @@ struct LeafArgs {
 struct MpArgs {
     double* X;
     const double* U;           // source rows U[lo, mid) (== X; Scheme 2: V = U_i + U_(i-1))
-    const double* rsrc;        // target R is read from here (== X except first touch)
+    const double* rsrc;        // target R is read from here (== X except first touch; null = zero)
     uint64_t N;
     uint64_t lo, mid, hi;      // source [lo, mid), target [mid, min(hi, N))
     int n, m, K, G;            // block size, branch length, branches, row pairs per CTA
@@ -212,6 +215,8 @@ cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int c
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
+int gen_terms(const RhsModesArgs& a);  // J of the separable RHS tables
+cudaError_t launch_gen_tables(const RhsModesArgs& a, double* A, double* T, cudaStream_t st);
 cudaError_t launch_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y,
                                    double beta, int block_mode, uint64_t vectors, cudaStream_t st);
 

@@ -135,8 +135,8 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
             for (int u = 0; u < 8; ++u) {
                 const int e = e0 + u * kLeafThreads + threadIdx.x;
                 const int q = e / HL, k2 = e - q * HL;
-                v[u] = e < total ? __ldcg(reinterpret_cast<const double2*>(src + (row0 + q) * N + t0) + k2)
-                                 : make_double2(0.0, 0.0);
+                v[u] = (e < total && src) ? __ldcg(reinterpret_cast<const double2*>(src + (row0 + q) * N + t0) + k2)
+                                          : make_double2(0.0, 0.0);
             }
             if (radd) {
 #pragma unroll
@@ -169,7 +169,8 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
         for (int u = 0; u < 8; ++u) {
             const int e = e0 + u * kLeafThreads + threadIdx.x;
             const int q = e / len, k = e - q * len;
-            v[u] = e < total ? src[(row0 + q) * N + t0 + k] + (radd ? radd[(row0 + q) * N + t0 + k] : 0.0) : 0.0;
+            v[u] = e < total ? (src ? src[(row0 + q) * N + t0 + k] : 0.0) + (radd ? radd[(row0 + q) * N + t0 + k] : 0.0)
+                             : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -306,6 +307,27 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         const bool valid = q < mreal;
 #pragma unroll
         for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? s_out[q * (L + 1) + k] : 0.0;
+    }
+    if (a.genA) {
+        // fused separable RHS (ft_solve_fast_modes): tile += sum_j A[row][j] T[pb][t][j]
+        // straight into the register window; T is warp-uniform (broadcast loads)
+        const int J = a.genJ;
+        const double* Tb = a.genT + ((uint64_t)pb * N + a.t0) * J;
+#pragma unroll 1
+        for (int j = 0; j < J; ++j) {
+            double av[NPT];
+#pragma unroll
+            for (int v = 0; v < NPT; ++v) {
+                const int q = tid * NPT + v;
+                av[v] = q < mreal ? __ldg(&a.genA[(rowb + q) * J + j]) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < L; ++k) {
+                const double t = k < len ? __ldg(&Tb[(uint64_t)k * J + j]) : 0.0;
+#pragma unroll
+                for (int v = 0; v < NPT; ++v) tile[v][k] = fma(av[v], t, tile[v][k]);
+            }
+        }
     }
     __syncthreads();
     if (stamp) a.dbg_clk[9] = clock64();
@@ -719,6 +741,30 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_correct(LeafArgs a) {
     correct_body<KIND, NPT, L>(a, s_dyn, s_dyn + (uint64_t)L * (2 * a.P + 1), false);
 }
 
+// L2 prefetch (evict_last) of the phase-2/3 tables this slab will read: its
+// rows of the injection response W and a share of the response table G, so
+// they arrive from L2 instead of HBM after the history products streamed
+// through the cache (ncu: long-scoreboard stalls in phases 2/3).
+__device__ __forceinline__ void prefetch_l2_last(const void* ptr) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ptr));
+}
+
+template <int L>
+__device__ __forceinline__ void prefetch_correct_tables(const LeafArgs& a) {
+    if (!a.resp_w || (a.dbg & 16)) return;
+    const int cta = blockIdx.x;
+    const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
+    const int P = a.P, m = a.slab;
+    const char* w = reinterpret_cast<const char*>(a.resp_w + ((uint64_t)pb * P + s) * 2 * L * 2 * P);
+    const int wbytes = 2 * L * 2 * P * 8;
+    for (int o = threadIdx.x * 128; o < wbytes; o += blockDim.x * 128) prefetch_l2_last(w + o);
+    // G tables [side][l][q] of the two slab kinds: lines spread over the CTAs of the problem
+    const char* g = reinterpret_cast<const char*>(a.resp_g + (uint64_t)pb * 2 * 2 * (uint64_t)m * L);
+    const int gbytes = 2 * 2 * m * L * 8;
+    const int c0 = cta - pb * a.P_local, nc = a.P_local;
+    for (int o = (c0 * blockDim.x + threadIdx.x) * 128; o < gbytes; o += nc * blockDim.x * 128) prefetch_l2_last(g + o);
+}
+
 // Single-GPU slab leaf in ONE cooperative kernel: phase 1, publish carries, a
 // grid barrier (all slabs co-resident), phases 2 + 3 on the resident tile.
 template <int KIND, int NPT, int L, bool PC>
@@ -726,6 +772,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
     double* s_c0 = s_dyn;
     double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
+    prefetch_correct_tables<L>(a);
     leaf_body<KIND, NPT, L, 1, PC>(a, s_x, false);
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_kernel(MpArgs a) {
             for (int q = 0; q < K / 2; ++q) {
                 const uint64_t t = a.mid + (uint64_t)q * m + r;
                 const bool okt = ok && t < tend;
-                r1[c][q] = okt ? a.rsrc[pi.row1 * N + t] : 0.0;
-                r2[c][q] = (okt && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + t] : 0.0;
+                r1[c][q] = (okt && a.rsrc) ? a.rsrc[pi.row1 * N + t] : 0.0;
+                r2[c][q] = (okt && pi.has2 && a.rsrc) ? a.rsrc[(pi.row1 + 1) * N + t] : 0.0;
             }
         }
 #pragma unroll
@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
 #pragma unroll
     for (int q = 0; q < K / 2; ++q) {
         const uint64_t t = a.mid + (uint64_t)q * m + r;
-        r1[q] = t < tend ? a.rsrc[row1 * N + t] : 0.0;
-        r2[q] = (t < tend && has2) ? a.rsrc[(row1 + 1) * N + t] : 0.0;
+        r1[q] = (t < tend && a.rsrc) ? a.rsrc[row1 * N + t] : 0.0;
+        r2[q] = (t < tend && has2 && a.rsrc) ? a.rsrc[(row1 + 1) * N + t] : 0.0;
     }
     const cplx* in = a.scratch + (uint64_t)pl * K * m + r;
     cplx wv[K];
@@ -407,8 +407,8 @@ __device__ __forceinline__ void mp1_last_prefetch(const MpArgs& a, const PairInf
     for (int p = 0; p < 8; ++p) {
         const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
         const bool ok = live && tt < tend;
-        r1[p] = ok ? a.rsrc[pi.row1 * a.N + tt] : 0.0;
-        r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * a.N + tt] : 0.0;
+        r1[p] = (ok && a.rsrc) ? a.rsrc[pi.row1 * a.N + tt] : 0.0;
+        r2[p] = (ok && pi.has2 && a.rsrc) ? a.rsrc[(pi.row1 + 1) * a.N + tt] : 0.0;
     }
     pass_twiddles<16>(w, a.tw, Q0 * 16, j);
 }
@@ -460,6 +460,9 @@ __device__ __forceinline__ void mp1_last_task(const MpArgs& a, cplx* buf, const 
 // the last pass -- are issued before the barrier that precedes the phase
 // (ncu: these L1/L2 round trips were the top long-scoreboard stalls).
 template <int LOGN>
+#ifndef FT_MP1G_MINB
+#define FT_MP1G_MINB 2
+#endif
 #ifndef FT_MP1_MINB
 #define FT_MP1_MINB 2
 #endif
@@ -617,7 +620,7 @@ __device__ __forceinline__ void mid_inv_g(cplx* buf, int total, const cplx* tw, 
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
+__global__ void __launch_bounds__(kMpThreads, FT_MP1G_MINB) mp1g_kernel(MpArgs a) {
     pdl_launch_dependents(a.pdl_trigger);
     pdl_wait();
     using PL = Plan1<LOGN>;
@@ -693,8 +696,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp1g_kernel(MpArgs a) {
     for (int p = 0; p < 8; ++p) {
         const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
         const bool ok = live && tt < tend;
-        r1[p] = ok ? a.rsrc[pi.row1 * N + tt] : 0.0;
-        r2[p] = (ok && pi.has2) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
+        r1[p] = (ok && a.rsrc) ? a.rsrc[pi.row1 * N + tt] : 0.0;
+        r2[p] = (ok && pi.has2 && a.rsrc) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
     }
     cplx w[16];
     pass_twiddles<16>(w, a.tw, n, j);
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
         const uint64_t row = row0 + r2;
         const bool ok = row < (uint64_t)a.rows;
         uu[i] = ok ? a.U[row * N + a.lo + j] : 0.0;
-        rv[i] = (ok && j < nt) ? a.rsrc[row * N + a.mid + j] : 0.0;
+        rv[i] = (ok && j < nt && a.rsrc) ? a.rsrc[row * N + a.mid + j] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {

@@ -274,3 +274,48 @@ def test_every_level_full_N(ft, oracle_mod, cid):
     ref = oracle_mod.direct(w, F, u0, phi)
     _, _, U, _ = _fast(ft, w, F, u0, phi)
     assert oracle_mod.relerr(U, ref) <= TOL
+
+
+@pytest.mark.parametrize("cid,kw,rhs_mode", [
+    (1, dict(time_steps=1000), 0),
+    (2, dict(time_steps=700, cells=33), 0),
+    (3, dict(time_steps=512, cells=17), 0),
+    (3, dict(time_steps=512, cells=17), 1),
+    (4, dict(time_steps=256, cells=3001), 0),     # multi-slab (fused cooperative) leaf, uneven slab
+    (4, dict(time_steps=128), 0),                 # full cfg4 width
+    (5, dict(time_steps=1024, batch=3), 0),
+], ids=["cfg1", "cfg2", "cfg3", "cfg3-corrected", "cfg4-multislab", "cfg4-fullM", "cfg5"])
+def test_fused_rhs_generation(ft, oracle_mod, cid, kw, rhs_mode):
+    """ft_solve_fast_modes (separable forcing generated inside the leaves, no RHS
+    array) agrees with ft_solve_fast on the ft_assemble_rhs_modes RHS to rounding
+    (the history accumulates from zero instead of from R: a different summation
+    order, not different arithmetic)."""
+    import torch
+
+    w = W.config(cid, **kw)
+    plan = ft.Plan(w.specs, rhs_mode=rhs_mode)
+    rhs = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.assemble_rhs_modes(rhs, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    U, _ = plan.solve_fast(rhs, torch.empty_like(rhs))
+    Ug = torch.empty_like(rhs)
+    _, rep = plan.solve_fast_modes(Ug, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    assert rep.kernel_launches > 0
+    err = oracle_mod.relerr(Ug.cpu().numpy(), U.cpu().numpy())
+    assert err <= 1e-12, f"rel err {err:.3e}"
+    # host output buffer, and the transport scheme (stencil leaf)
+    Uh = np.empty(plan.shape)
+    plan.solve_fast_modes(Uh, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    assert np.array_equal(Uh, Ug.cpu().numpy())
+
+
+def test_fused_rhs_generation_transport(ft, oracle_mod):
+    import torch
+
+    w = W.transport(0.45, 2048, 129, 0.6)
+    plan = ft.Plan(w.specs)
+    rhs = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.assemble_rhs_modes(rhs, w.a, w.k, w.p, w.trig, w.u0amp, None)
+    U, _ = plan.solve_fast(rhs, torch.empty_like(rhs))
+    Ug = torch.empty_like(rhs)
+    plan.solve_fast_modes(Ug, w.a, w.k, w.p, w.trig, w.u0amp, None)
+    assert oracle_mod.relerr(Ug.cpu().numpy(), U.cpu().numpy()) <= 1e-12
