@@ -40,14 +40,16 @@ def peaks():
 
 
 # DRAM bytes / algorithmic bytes of one history-product launch, measured with
-# ncu --set full on B200 (profiles/ncu_r01/README.md): direct kernel (n <= 128),
-# single-CTA FFT kernel (256 <= n <= 8192), 4-CTA cluster (n = 16384), split
-# A + B kernels with the branch scratch round trip (n >= 32768).
-NCU_DRAM_OVER_ALG = {"direct": 0.67, "single": 0.80, "cluster": 1.00, "split": 2.27}
+# ncu --set full on B200 (profiles/ncu_r01/kernels.json): direct kernel
+# (n <= 128: 0.67), group-private single-CTA FFT (256 <= n <= 4096: 0.81 at
+# n = 256, 0.90 at n = 512), 2- and 4-CTA clusters (n = 8192, 16384: 1.00),
+# split K-branch kernels + combine with the branch scratch round trip
+# (n >= 32768: 2.15 at K = 8; the pre-folded K = 16 level is taken equal).
+NCU_DRAM_OVER_ALG = {"direct": 0.67, "single": 0.86, "cluster": 1.00, "split": 2.15}
 
 
 def mp_family(n: int) -> str:
-    return "direct" if n <= 128 else "single" if n <= 8192 else "cluster" if n <= 16384 else "split"
+    return "direct" if n <= 128 else "single" if n <= 4096 else "cluster" if n <= 16384 else "split"
 
 
 def bytes_per_unknown(N: int) -> float:
