@@ -1065,19 +1065,9 @@ int ft_assemble_rhs_modes(const ft_plan* p, int nmodes, const double* a, const d
 
 // Fast solve with pinned host buffers: chunked H2D of R and D2H of U overlap
 // the solve (StreamIO).  Pageable host buffers take the serial path below.
-static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool stream_rhs,
-                          std::chrono::steady_clock::time_point t_start) {
-    const uint64_t N = p->N, rows = rows_of(p);
-    const size_t bytes = sizeof(double) * rows * N;
-    const cudaStream_t st = p->stream;
-    const bool u_dev = is_device_ptr(u);
-    double* X = u;
-    if (!u_dev) {
-        int rc = ensure_work(p);
-        if (rc) return rc;
-        X = p->work_d;
-    }
-    StreamIO io;
+// Chunking and copy streams of the streamed host paths.
+static int stream_setup(ft_plan* p, StreamIO& io) {
+    const uint64_t N = p->N;
     // chunk: wide enough for efficient 2D DMA rows, small enough for a short fill/drain
     uint64_t C = getenv("FT_STREAM_CHUNK") ? (uint64_t)atoll(getenv("FT_STREAM_CHUNK")) : 2048;  // B200 PCIe: 16 KB rows best (measured 256..4096)
     C = std::max<uint64_t>((C + p->L - 1) / p->L * p->L, (uint64_t)p->L);
@@ -1094,6 +1084,27 @@ static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* r
         p->h2d_ev.push_back(e1);
         p->d2h_ev.push_back(e2);
     }
+    return FT_OK;
+}
+
+static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* rep, bool stream_rhs,
+                          std::chrono::steady_clock::time_point t_start) {
+    const uint64_t N = p->N, rows = rows_of(p);
+    const size_t bytes = sizeof(double) * rows * N;
+    const cudaStream_t st = p->stream;
+    const bool u_dev = is_device_ptr(u);
+    double* X = u;
+    if (!u_dev) {
+        int rc = ensure_work(p);
+        if (rc) return rc;
+        X = p->work_d;
+    }
+    StreamIO io;
+    {
+        int rc = stream_setup(p, io);
+        if (rc) return rc;
+    }
+    const uint64_t nch = (N + io.C - 1) / io.C;
     FT_CUDA(cudaEventRecord(p->ev0, st));
     const double* src = rhs;
     if (stream_rhs) {
@@ -1342,9 +1353,21 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
     }
     uint64_t launches = 0;
     FT_CUDA(cudaEventRecord(p->ev0, st));
-    if ((rc = launch_fast(p, X, nullptr, &gen, &launches))) return rc;
-    FT_CUDA(cudaEventRecord(p->ev1, st));
-    if (!u_dev) FT_CUDA(cudaMemcpyAsync(u, X, sizeof(double) * rows_of(p) * p->N, cudaMemcpyDeviceToHost, st));
+    if (!u_dev && is_pinned_host(u) && !getenv("FT_NO_STREAM")) {
+        // pinned host output: finished chunks of U leave on the copy stream while the
+        // solve continues (the only PCIe traffic of this call besides the mode arguments)
+        StreamIO io;
+        if ((rc = stream_setup(p, io))) return rc;
+        io.u_host = u;
+        if ((rc = run_fast(p, X, nullptr, &launches, nullptr, &io, &gen))) return rc;
+        FT_CUDA(cudaEventRecord(p->ev1, st));
+        FT_CUDA(cudaStreamSynchronize(st));
+        FT_CUDA(cudaStreamSynchronize(p->d2h_st));
+    } else {
+        if ((rc = launch_fast(p, X, nullptr, &gen, &launches))) return rc;
+        FT_CUDA(cudaEventRecord(p->ev1, st));
+        if (!u_dev) FT_CUDA(cudaMemcpyAsync(u, X, sizeof(double) * rows_of(p) * p->N, cudaMemcpyDeviceToHost, st));
+    }
     FT_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
     FT_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
