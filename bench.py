@@ -355,9 +355,13 @@ def run_ours(args, world, rank, local):
                 plan.solve_fast_modes(un, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
             em_s = (time.perf_counter() - t0) / args.e2e_steps
             arg_bytes = 8 * (wl.a.size + wl.k.size + wl.p.size + wl.trig.size + wl.B * 3)
-            e2e["modes"] = {"value": total_unknowns / em_s, "unit": "unknowns/s", "ms_per_step": 1e3 * em_s,
-                            "h2d_bytes_per_step": int(arg_bytes), "d2h_bytes_per_step": nbytes,
-                            "path": "ft_solve_fast_modes C ABI, pinned host output"}
+            # BASELINE config 4's input IS the 8-mode forcing (seeded coefficients), and the
+            # reference's solve(spec) takes it as a callback: this call is the headline e2e;
+            # the RHS-array call is kept beside it
+            e2e = {"value": total_unknowns / em_s, "unit": "unknowns/s", "h2d_bytes_per_step": int(arg_bytes),
+                   "d2h_bytes_per_step": nbytes, "ms_per_step": 1e3 * em_s, "steps": args.e2e_steps,
+                   "path": "ft_solve_fast_modes C ABI: forcing modes in (host), U out to pinned host memory",
+                   "array_rhs": e2e}
         del h_rhs, h_u
 
     cpu = None
