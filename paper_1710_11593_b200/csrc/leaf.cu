@@ -23,7 +23,13 @@
 //     space-time response tables GL, GR: x += sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l).
 #include "internal.cuh"
 
+#ifndef FT_LEAF_UNROLL
+#define FT_LEAF_UNROLL 1  // step-loop unroll: 1 measured 403 ms vs 408 (2) and 412 (4) on cfg4 (instruction fetch)
+#endif
+
 namespace ftb {
+
+constexpr int kLeafUnroll = FT_LEAF_UNROLL;
 
 // in-leaf history weights col[1..L) per problem, read through the constant
 // cache (CTA-uniform: the compiler keeps them in uniform registers)
@@ -350,7 +356,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     // the remaining in-leaf steps (no unrolling over k: the body stays small
     // enough for the instruction cache).  Unrolled by two so the off-critical
     // push FMAs of step k can be scheduled under the scan latency of step k+1.
-#pragma unroll 2
+#pragma unroll kLeafUnroll
     for (int k = 0; k < len; ++k) {
         const int par = k & 1;
         double x[NPT];
