@@ -473,8 +473,15 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     // leaf configuration
     const int nodes = p->nodes;
     p->local_nodes = nodes;
+    // problems at least this wide use the slab (SPIKE) leaf; narrower ones one CTA (tuning knob)
+    // (513: config 3, 1024 nodes, 114 -> 92 ms as 2 slabs with L = 32 instead of one CTA with L = 16)
+    const int slab_min = getenv("FT_SLAB_MIN") ? atoi(getenv("FT_SLAB_MIN")) : 513;
     if (p->kind == SK_DIAG) {
         p->npt = 1; p->L = 32; p->threads = 32; p->slab = 1; p->P = 1;
+    } else if (nodes >= slab_min && !p->stencil) {
+        p->npt = 2; p->L = 32; p->threads = 256; p->slab = 512;
+        p->P = (nodes + p->slab - 1) / p->slab;
+        p->multi = true;
     } else if (nodes <= 256) {
         p->npt = 1; p->L = 32; p->threads = ((nodes + 31) / 32) * 32; p->slab = nodes; p->P = 1;
     } else if (nodes <= 512) {

@@ -354,8 +354,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     // Rolling window: tile[v][i] holds the right-hand side of step k + i; each
     // step shifts it down by one register while pushing the new solution into
     // the remaining in-leaf steps (no unrolling over k: the body stays small
-    // enough for the instruction cache).  Unrolled by two so the off-critical
-    // push FMAs of step k can be scheduled under the scan latency of step k+1.
+    // enough for the instruction cache -- unrolling by 2 or 4 measured slower).
 #pragma unroll kLeafUnroll
     for (int k = 0; k < len; ++k) {
         const int par = k & 1;

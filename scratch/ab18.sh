@@ -1,0 +1,5 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/ab18_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ab18_pytest.log
+timeout 300 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu --no-fused > gpurun_out/ab18_c4.json 2>gpurun_out/ab18_c4.err
+timeout 300 python bench.py --config 3 --steps 5 --warmup 3 --no-cpu > gpurun_out/ab18_c3.json 2>gpurun_out/ab18_c3.err
