@@ -228,7 +228,9 @@ def run_ours(args, world, rank, local):
         # products, one carry all-gather (NCCL) per leaf -- strong scaling
         from paper_1710_11593_b200.parallel import ShardedPlan
 
-        plan = ShardedPlan(wl.specs[0], rank, world, device=local)
+        # FT_P2P_EXCHANGE=1: the leaf kernels exchange the carries over NVLink peer memory
+        # (ft_p2p_connect) instead of the NCCL hook -- opt-in, not yet run on a multi-GPU box
+        plan = ShardedPlan(wl.specs[0], rank, world, device=local, p2p=os.environ.get("FT_P2P_EXCHANGE") == "1")
         stream = plan.stream
     else:
         # independent problems (config 5: shard the batch) or replicas

@@ -155,6 +155,15 @@ int ft_setup_partitioned(const ft_problem* problem, const ft_options* options, i
                          ft_plan** out);
 int ft_set_exchange(ft_plan* plan, ft_exchange_fn exchange, void* user, double* send_device,
                     double* recv_device);
+/* Alternative to the hook (opt-in): the leaf kernel exchanges the carries itself
+ * over NVLink peer memory.  Each rank allocates its exchange block and exports a
+ * CUDA IPC handle (64 bytes) with ft_p2p_handle; the caller all-gathers the
+ * handles (rank-major) and passes them to ft_p2p_connect on every rank.  From
+ * then on every leaf is one cooperative kernel per rank: phase 1, stores of the
+ * carries into every rank's block, a system-scope arrival counter, phases 2/3.
+ * All ranks must run the same sequence of fast solves. */
+int ft_p2p_handle(ft_plan* plan, void* handle_out);
+int ft_p2p_connect(ft_plan* plan, const void* handles);
 int ft_column(const ft_plan* plan, uint64_t problem, double* col_host);
 
 int ft_assemble_rhs(const ft_plan* plan, ft_forcing_fn forcing, ft_initial_fn u0,

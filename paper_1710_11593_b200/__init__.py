@@ -94,7 +94,7 @@ _lib = None
 
 ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exchange", "ft_plan_get_info", "ft_column", "ft_assemble_rhs",
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
-               "ft_solve_fast_modes",
+               "ft_solve_fast_modes", "ft_p2p_handle", "ft_p2p_connect",
                "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy",
                "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec")
 
@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
         L.ft_solve_fast.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_fast_modes.argtypes = [P, I, P, P, P, P, P, P, P, C.POINTER(_Report)]
+        L.ft_p2p_handle.argtypes = [P, P]
+        L.ft_p2p_connect.argtypes = [P, P]
         L.ft_set_stream.argtypes = [P, P]
         L.ft_profile_fast.argtypes = [P, P, P, C.POINTER(_OpTime), U64, C.POINTER(U64)]
         L.ft_schedule.argtypes = [U64, U64, C.POINTER(_OpTime), U64, C.POINTER(U64)]

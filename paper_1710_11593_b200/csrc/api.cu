@@ -83,6 +83,11 @@ struct ft_plan {
     void* exchange_user = nullptr;
     double* xsend_d = nullptr;  // caller-provided (partitioned) phase-1 carry buffer
     bool own_xch = true;
+    // device-side exchange over NVLink peer memory (ft_p2p_handle / ft_p2p_connect)
+    bool p2p = false;
+    void* p2p_block = nullptr;                 // this rank's exchange block (kP2pHeader + receive buffers)
+    std::vector<void*> p2p_opened;             // peers' blocks mapped through CUDA IPC
+    unsigned long long* p2p_peers_d = nullptr; // [world] block bases, device array
     unsigned* bar_d = nullptr;  // fused slab leaf grid barrier
     cplx* mpscratch_d = nullptr;  // split K-branch history products
     bool split_k = true;
@@ -677,6 +682,9 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     uint64_t nl = 0;
     unsigned leaf_index = 0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
+    int leaves_total = 0;
+    for (const Op& o : p->ops) leaves_total += o.kind == OP_LEAF ? 1 : 0;
+    if (p->p2p) FT_CUDA(launch_p2p_epoch(reinterpret_cast<unsigned*>((char*)p->p2p_block + 8), st));
     for (size_t oi = 0; oi < p->ops.size(); ++oi) {
         const Op& op = p->ops[oi];
         if (evs) FT_CUDA(cudaEventRecord((*evs)[oi], st));
@@ -727,12 +735,21 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.bar = p->bar_d;
             a.bar_target = (unsigned)(leaf_index + 1) * (unsigned)(p->B * p->P_local);
             ++leaf_index;
-            if (p->multi && p->part_world == 1 && p->fused_leaf) {
+            a.p2p_peers = p->p2p_peers_d;
+            a.p2p_epoch = p->p2p ? reinterpret_cast<const unsigned*>((const char*)p->p2p_block + 8) : nullptr;
+            a.p2p_world = p->part_world;
+            a.p2p_leaf = (int)leaf_index - 1;
+            a.p2p_leaves = leaves_total;
+            if (p->p2p) {  // exchange inside the kernel over peer memory: no hook, no second kernel
+                a.xch = reinterpret_cast<double*>((char*)p->p2p_block + kP2pHeader) +
+                        (size_t)(a.p2p_leaf & 1) * p->P * p->L * 2;
+                FT_CUDA(launch_leaf_p2p(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
+            } else if (p->multi && p->part_world == 1 && p->fused_leaf) {
                 FT_CUDA(launch_leaf_fused(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
             } else {
                 FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P_local, p->threads, st));
             }
-            if (p->multi && !(p->part_world == 1 && p->fused_leaf)) {
+            if (p->multi && !p->p2p && !(p->part_world == 1 && p->fused_leaf)) {
                 if (p->part_world > 1) {  // one carry all-gather per leaf (caller's collective)
                     if (!p->exchange)
                         return set_err(FT_EINVAL, "partitioned plan: no exchange hook (ft_set_exchange)");
@@ -900,6 +917,50 @@ int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options*
 int ft_setup_partitioned(const ft_problem* problem, const ft_options* options, int rank, int world,
                          ft_plan** out) {
     return setup_impl(problem, 1, options, out, rank, world);
+}
+
+int ft_p2p_handle(ft_plan* p, void* handle_out) {
+    if (!p || !handle_out) return set_err(FT_EINVAL, "ft_p2p_handle: null argument");
+    if (p->part_world <= 1 || !p->multi || p->B != 1) return set_err(FT_EINVAL, "ft_p2p_handle: plan is not partitioned");
+    FT_CUDA(cudaSetDevice(p->device));
+    if (!p->p2p_block) {
+        const size_t bytes = kP2pHeader + sizeof(double) * 2 * (size_t)p->P * p->L * 2;
+        FT_CUDA(cudaMalloc(&p->p2p_block, bytes));
+        FT_CUDA(cudaMemset(p->p2p_block, 0, bytes));
+    }
+    cudaIpcMemHandle_t h;
+    FT_CUDA(cudaIpcGetMemHandle(&h, p->p2p_block));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return FT_OK;
+}
+
+int ft_p2p_connect(ft_plan* p, const void* handles) {
+    if (!p || !handles) return set_err(FT_EINVAL, "ft_p2p_connect: null argument");
+    if (!p->p2p_block) return set_err(FT_EINVAL, "ft_p2p_connect: call ft_p2p_handle first");
+    FT_CUDA(cudaSetDevice(p->device));
+    std::vector<unsigned long long> bases(p->part_world);
+    for (int r = 0; r < p->part_world; ++r) {
+        if (r == p->part_rank) {
+            bases[r] = (unsigned long long)(uintptr_t)p->p2p_block;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, (const char*)handles + (size_t)r * sizeof(h), sizeof(h));
+        void* ptr = nullptr;
+        FT_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        p->p2p_opened.push_back(ptr);
+        bases[r] = (unsigned long long)(uintptr_t)ptr;
+    }
+    if (!p->p2p_peers_d) FT_CUDA(cudaMalloc(&p->p2p_peers_d, sizeof(unsigned long long) * p->part_world));
+    FT_CUDA(cudaMemcpy(p->p2p_peers_d, bases.data(), sizeof(unsigned long long) * p->part_world,
+                       cudaMemcpyHostToDevice));
+    int dev_sms = 0;
+    FT_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
+    if (p->P_local > dev_sms) return set_err(FT_EINVAL, "ft_p2p_connect: more slabs per rank than SMs");
+    p->p2p = true;
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+    return FT_OK;
 }
 
 int ft_set_exchange(ft_plan* p, ft_exchange_fn fn, void* user, double* send_device, double* recv_device) {
@@ -1152,7 +1213,7 @@ static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* r
 // rank; keyed by the buffers and the fused-RHS tables), else launched directly.
 static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* gen, uint64_t* launches) {
     const cudaStream_t st = p->stream;
-    const bool use_graph = p->part_world == 1 && !getenv("FT_NO_GRAPH");
+    const bool use_graph = (p->part_world == 1 || p->p2p) && !getenv("FT_NO_GRAPH");
     if (!use_graph) return run_fast(p, X, src, launches, nullptr, nullptr, gen);
     const void* gkey = gen ? (const void*)gen->A : nullptr;
     if (!p->graph || p->graph_X != X || p->graph_src != src || p->graph_gen != gkey) {
@@ -1476,6 +1537,9 @@ void ft_destroy(ft_plan* p) {
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     if (p->rdev_d) cudaFree(p->rdev_d);
+    for (void* q : p->p2p_opened) cudaIpcCloseMemHandle(q);
+    if (p->p2p_block) cudaFree(p->p2p_block);
+    if (p->p2p_peers_d) cudaFree(p->p2p_peers_d);
     for (cudaEvent_t e : p->h2d_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : p->d2h_ev) cudaEventDestroy(e);
     if (p->h2d_st) cudaStreamDestroy(p->h2d_st);

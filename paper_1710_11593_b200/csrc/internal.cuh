@@ -143,6 +143,10 @@ struct LeafArgs {
     const double* genA;        // fused separable RHS (ft_solve_fast_modes): [rows][genJ] node factors
     const double* genT;        //   [B][N][genJ] step factors; R = sum_j genA * genT added at staging
     int genJ;                  //   (null genA: R comes from src)
+    // device-side carry exchange over NVLink peer memory (partitioned plans, opt-in):
+    const unsigned long long* p2p_peers;  // [world] base of every rank's exchange block (peer-mapped)
+    const unsigned* p2p_epoch;            // this rank's solve counter (incremented per solve)
+    int p2p_world, p2p_leaf, p2p_leaves;  // ranks, leaf index in the solve, leaves per solve
     int kc_valid;              // kc holds problem 0's leaf constants (single-problem plans)
     double kc[kKcLen];         // see kKc* (kernel parameter: constant-bank operands)
 };
@@ -212,6 +216,11 @@ cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a,
 cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double* W, cudaStream_t st);
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st);
+// exchange block layout: [0] uint64 arrival counter, [8] uint32 solve epoch, [64..) receive
+// buffers [2 parities][P][L][2] doubles
+constexpr size_t kP2pHeader = 64;
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);

@@ -792,6 +792,55 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     correct_body<KIND, NPT, L>(a, s_c0, s_x, true);
 }
 
+// Partitioned slab leaf with the carry exchange done by the kernel itself over
+// NVLink peer memory (opt-in, ft_p2p_connect): phase 1; every CTA stores its
+// slab's 2L carries into every rank's receive buffer (parity = leaf index & 1,
+// so a fast rank never overwrites carries a slow rank is still reading: it
+// cannot pass the next leaf's barrier before that rank arrives), fences at
+// system scope and bumps every rank's arrival counter; one thread per CTA
+// waits until its own counter shows all world x P_local slabs of this leaf;
+// phases 2/3 read the gathered carries locally.  Counters are cumulative over
+// solves (epoch kernel at each solve start), so no reset race exists.
+template <int KIND, int NPT, int L, bool PC>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused_p2p(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    double* s_c0 = s_dyn;
+    double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
+    leaf_body<KIND, NPT, L, 1, PC>(a, s_x, false);  // carries -> a.xsend[cta] (local)
+    __syncthreads();
+    const int cta = blockIdx.x, s = a.s_begin + cta;
+    const double* mine = a.xsend + (uint64_t)cta * L * 2;
+    const size_t par_off = (size_t)(a.p2p_leaf & 1) * a.P * L * 2;
+    for (int r = 0; r < a.p2p_world; ++r) {
+        double* dst = reinterpret_cast<double*>(a.p2p_peers[r] + kP2pHeader) + par_off + (uint64_t)s * L * 2;
+        for (int i = threadIdx.x; i < 2 * L; i += blockDim.x) dst[i] = __ldcg(&mine[i]);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < a.p2p_world; ++r)
+            atomicAdd_system(reinterpret_cast<unsigned long long*>(a.p2p_peers[r]), 1ull);
+        const unsigned epoch = *a.p2p_epoch;  // 1-based: solves started on this rank
+        const unsigned long long per_leaf = (unsigned long long)a.p2p_world * a.P_local;
+        const unsigned long long target =
+            ((unsigned long long)(epoch - 1) * a.p2p_leaves + a.p2p_leaf + 1) * per_leaf;
+        const unsigned long long* own = reinterpret_cast<const unsigned long long*>(a.p2p_peers[a.s_begin / a.P_local]);
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(own) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+    correct_body<KIND, NPT, L>(a, s_c0, s_x, true);  // a.xch = this rank's receive buffer (parity)
+}
+
+__global__ void p2p_epoch_kernel(unsigned* epoch) { *epoch += 1u; }
+
+cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st) {
+    p2p_epoch_kernel<<<1, 1, 0, st>>>(epoch);
+    return cudaGetLastError();
+}
+
 // ---- host launch -------------------------------------------------------------
 
 template <int KIND, int NPT, int L>
@@ -851,6 +900,38 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
     cfg.numAttrs = 1;
     return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, true>, a)
                       : cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, false>, a);
+}
+
+template <int KIND, int NPT, int L>
+static cudaError_t launch_p2p_t(const LeafArgs& a, int ctas, cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
+    static bool attr = false;
+    if (!attr) {
+        const int mx = (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1)));
+        cudaFuncSetAttribute(leaf_fused_p2p<KIND, NPT, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_fused_p2p<KIND, NPT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLeafThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute coop[1];
+    coop[0].id = cudaLaunchAttributeCooperative;  // every slab CTA of this rank co-resident
+    coop[0].val.cooperative = 1;
+    cfg.attrs = coop;
+    cfg.numAttrs = 1;
+    return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused_p2p<KIND, NPT, L, true>, a)
+                      : cudaLaunchKernelEx(&cfg, leaf_fused_p2p<KIND, NPT, L, false>, a);
+}
+
+cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
+    if (npt == 2 && L == 32) {
+        if (kind == SK_TRIDIAG) return launch_p2p_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
+        if (kind == SK_UPWIND) return launch_p2p_t<SK_UPWIND, 2, 32>(a, ctas, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {

@@ -71,7 +71,8 @@ class ShardedPlan(Plan):
     called once per leaf and must all-gather `count` doubles per rank from
     `self.send` into `self.recv` on `self.stream`."""
 
-    def __init__(self, spec, rank: int, world: int, exchange_factory=None, device: int = -1, **kw):
+    def __init__(self, spec, rank: int, world: int, exchange_factory=None, device: int = -1, p2p: bool = False,
+                 **kw):
         super().__init__(spec, partition=(rank, world), device=device, **kw)
         self.rank, self.world = rank, world
         P_local, L = int(self.info.slabs_local), int(self.info.leaf)
@@ -95,3 +96,18 @@ class ShardedPlan(Plan):
 
         self._hook = EXCHANGE_FN(hook)  # keep alive
         _check(lib().ft_set_exchange(self._h, self._hook, None, self.send.data_ptr(), self.recv.data_ptr()))
+        if p2p:
+            self.connect_peers()
+
+    def connect_peers(self, group=None) -> None:
+        """Switch to the in-kernel exchange over NVLink peer memory: all-gather the
+        ranks' CUDA IPC handles (any torch.distributed backend) and map them."""
+        import torch.distributed as dist
+
+        h = (C.c_ubyte * 64)()
+        _check(lib().ft_p2p_handle(self._h, h))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        blob = b"".join(handles)
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(lib().ft_p2p_connect(self._h, buf))
