@@ -308,6 +308,21 @@ def test_fused_rhs_generation(ft, oracle_mod, cid, kw, rhs_mode):
     assert np.array_equal(Uh, Ug.cpu().numpy())
 
 
+def test_fused_rhs_streamed_to_pinned_host(ft):
+    """ft_solve_fast_modes into pinned host memory streams U back chunk by chunk
+    while the solve runs: bitwise equal to the device-buffer call (same kernels,
+    same order)."""
+    import torch
+
+    w = W.config(4, time_steps=4096 + 32, cells=1537)  # 3 slabs, ragged chunk tail
+    plan = ft.Plan(w.specs)
+    Ud = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.solve_fast_modes(Ud, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    Uh = torch.empty(plan.shape, dtype=torch.float64, pin_memory=True)
+    plan.solve_fast_modes(Uh.numpy(), w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    assert torch.equal(Uh, Ud.cpu())
+
+
 def test_fused_rhs_generation_transport(ft, oracle_mod):
     import torch
 
