@@ -334,3 +334,18 @@ def test_fused_rhs_generation_transport(ft, oracle_mod):
     Ug = torch.empty_like(rhs)
     plan.solve_fast_modes(Ug, w.a, w.k, w.p, w.trig, w.u0amp, None)
     assert oracle_mod.relerr(Ug.cpu().numpy(), U.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("cid,kw", [
+    (5, dict(time_steps=256, cells=1001, batch=3)),   # batched multi-slab: per-problem constants path
+    (3, dict(time_steps=200, cells=700)),             # wave scheme, 2 uneven slabs
+    (4, dict(time_steps=33, cells=600)),              # one leaf + a 1-step leaf, 2 slabs
+    (2, dict(time_steps=1, cells=17)),                # a single step
+    (1, dict(time_steps=31)),                         # a single partial leaf
+])
+def test_edge_shapes(ft, oracle_mod, cid, kw):
+    w = W.config(cid, **kw)
+    F, u0, phi = _inputs(oracle_mod, w)
+    ref = oracle_mod.direct(w, F, u0, phi)
+    _, _, U, _ = _fast(ft, w, F, u0, phi)
+    assert oracle_mod.relerr(U, ref) <= TOL
