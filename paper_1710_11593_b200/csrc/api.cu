@@ -540,6 +540,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         const double* lp0 = lampow.data();
         auto lpk = [&](int k) { return lp0[std::min(k, p->lp_stride - 1)]; };
         for (int j = 0; j < 32; ++j) p->kc_h[j] = p->leafcol_h[j];
+        for (int j = 0; j < 32; ++j) p->kc_h[kKcCol2 + j] = (uint64_t)(32 + j) < N ? p->col_h[32 + j] : 0.0;
         for (int d = 0; d < 5; ++d) p->kc_h[kKcPow + d] = lpk(p->npt << d);
         p->kc_h[kKcLamW] = lpk(32 * p->npt);
         p->kc_h[kKcLam] = p->pc_h[0].lam;
@@ -681,6 +682,10 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     if (cap == cudaStreamCaptureStatusNone) FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     uint64_t nl = 0;
     unsigned leaf_index = 0;
+    // the n = 64 history products fold into the next (cooperative slab) leaf
+    const bool fuse0 = p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && !io && !gen &&
+                       !p->stencil && getenv("FT_NO_FUSE0") == nullptr;
+    bool pend0 = false, pend0_first = false;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
     int leaves_total = 0;
     for (const Op& o : p->ops) leaves_total += o.kind == OP_LEAF ? 1 : 0;
@@ -696,6 +701,9 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             const bool defer = io && io->defer;
             a.src = (op.first && !defer) ? rhs : X;
             a.radd = defer ? io->rdev : nullptr;
+            a.fuse0 = (fuse0 && pend0) ? 1 : 0;
+            if (a.fuse0 && pend0_first) a.src = rhs;  // the skipped product was this tile's first touch
+            pend0 = false;
             a.genA = gen ? gen->A : nullptr;
             a.genT = gen ? gen->T : nullptr;
             a.genJ = gen ? gen->J : 0;
@@ -770,6 +778,11 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
                 }
             }
         } else {
+            if (fuse0 && op.level == 0 && oi + 1 < p->ops.size() && p->ops[oi + 1].kind == OP_LEAF) {
+                pend0 = true;  // applied by the next leaf kernel
+                pend0_first = op.first;
+                continue;
+            }
             const Level& lv = p->levels[op.level];
             MpArgs a;
             a.X = X;

@@ -32,7 +32,8 @@ constexpr int kLeafThreads = 256;
 // LeafArgs::kc layout (single-problem plans): in-leaf weights col[0..32), then
 // the uniform scan multipliers lam^(NPT 2^d) (d < 5), lam^(32 NPT), lam,
 // lam^(v+1) and lam^(NPT-v) (v < 8).
-constexpr int kKcPow = 32, kKcLamW = 37, kKcLam = 38, kKcV1 = 40, kKcNv = 48, kKcLen = 56;
+constexpr int kKcPow = 32, kKcLamW = 37, kKcLam = 38, kKcV1 = 40, kKcNv = 48, kKcCol2 = 56, kKcLen = 88;
+// (kKcCol2: col[32..64), the far half of the level-0 history window fused into the leaf)
 constexpr int kMaxSlabs = 160;
 constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in constant memory)  // slabs per problem in the multi-slab leaf
 constexpr int kMpThreads = 256;
@@ -147,6 +148,8 @@ struct LeafArgs {
     const unsigned long long* p2p_peers;  // [world] base of every rank's exchange block (peer-mapped)
     const unsigned* p2p_epoch;            // this rank's solve counter (incremented per solve)
     int p2p_world, p2p_leaf, p2p_leaves;  // ranks, leaf index in the solve, leaves per solve
+    int fuse0;                 // slab leaf applies the n = 64 history product from the previous leaf
+                               // (X[., t0-32, t0) -> this tile) itself; its launch is skipped
     int kc_valid;              // kc holds problem 0's leaf constants (single-problem plans)
     double kc[kKcLen];         // see kKc* (kernel parameter: constant-bank operands)
 };

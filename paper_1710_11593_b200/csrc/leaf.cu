@@ -314,6 +314,35 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 #pragma unroll
         for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? s_out[q * (L + 1) + k] : 0.0;
     }
+    if constexpr (PC && MODE == 1) {
+        if (a.fuse0) {
+            // level-0 history product (n = 64) of the previous leaf onto this one:
+            // tile[v][k] -= sum_j col[32 + k - j] U[row][t0 - 32 + j] (lags 1..63), with the
+            // previous leaf's U staged through s_out (free until the step loop writes it)
+            __syncthreads();
+            stage_rows<L>(s_out, a.X, nullptr, rowb, N, a.t0 - L, mreal, L);
+            __syncthreads();
+#pragma unroll
+            for (int v = 0; v < NPT; ++v) {
+                const int q = tid * NPT + v;
+                if (q >= mreal) continue;
+                double u[L];
+#pragma unroll
+                for (int jj = 0; jj < L; ++jj) u[jj] = s_out[q * (L + 1) + jj];
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int jj = 0; jj < L; ++jj) {
+                        const int lag = L + k - jj;  // 1 .. 2L-1
+                        const double c = lag < L ? a.kc[lag] : a.kc[kKcCol2 + lag - L];
+                        acc = fma(c, u[jj], acc);
+                    }
+                    tile[v][k] -= acc;
+                }
+            }
+        }
+    }
     if (a.genA) {
         // fused separable RHS (ft_solve_fast_modes): tile += sum_j A[row][j] T[pb][t][j]
         // straight into the register window; T is warp-uniform (broadcast loads)
