@@ -22,6 +22,8 @@
  *                                 lower_toeplitz_forward_solve()    src/toeplitz.cpp:169-186
  *   ft_solve_fast              <- solve(spec, SolveMethod::Fast)    src/schemes.cpp:464-474, :353-369,
  *                                                                    :233-257
+ *   ft_solve_fast_modes        <- the same, with the forcing callback evaluated inside the solve
+ *                                 (schemes.cpp:401-408 / :300-306 / :183-187) for separable forcings
  *                                 (GMRES + FFT matvec, src/krylov.cpp:107-223, replaced by a
  *                                 time-axis divide-and-conquer; same system, same answer)
  *   ft_setup_toeplitz          <- ToeplitzOperator::lower_triangular() include/fractime/toeplitz.hpp:33
