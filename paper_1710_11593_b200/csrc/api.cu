@@ -683,8 +683,9 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     uint64_t nl = 0;
     unsigned leaf_index = 0;
     // the n = 64 history products fold into the next (cooperative slab) leaf
-    const bool fuse0 = p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && !io && !gen &&
-                       !p->stencil && getenv("FT_NO_FUSE0") == nullptr;
+    // (wide problems only: for config 3's two slabs the standalone product is cheaper, 100 vs 102 ms)
+    const bool fuse0 = p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= 8 &&
+                       !io && !gen && !p->stencil && getenv("FT_NO_FUSE0") == nullptr;
     bool pend0 = false, pend0_first = false;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
     int leaves_total = 0;
