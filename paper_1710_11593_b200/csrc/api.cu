@@ -64,6 +64,7 @@ struct ft_plan {
     int rhs_mode = 0;
     bool custom = false;  // ft_setup_toeplitz plan (caller's columns, no RHS assembly)
     bool stencil = false; // Scheme 2: history products and in-leaf history act on U_i + U_(i-1)
+    bool last_fuse0 = false;  // the last run_fast folded the n = 64 products into the leaves
     double* vsrc_d = nullptr;  // Scheme 2: V = U_i + U_(i-1) (product sources), rows x N
     int J = 1;
     int device = 0;
@@ -687,6 +688,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     const bool fuse0 = p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= 8 &&
                        !io && !gen && !p->stencil && getenv("FT_NO_FUSE0") == nullptr;
     bool pend0 = false, pend0_first = false;
+    p->last_fuse0 = fuse0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
     int leaves_total = 0;
     for (const Op& o : p->ops) leaves_total += o.kind == OP_LEAF ? 1 : 0;
@@ -1535,6 +1537,13 @@ int ft_profile_fast(ft_plan* p, const double* rhs, double* u, ft_op_time* out, u
             o.len = tend - op.mid;
             o.bytes = 8ull * rows * h + 16ull * rows * o.len;  // read U half, read+write R half
         }
+    }
+    if (p->last_fuse0) {  // folded n = 64 products: their bytes belong to the next leaf's launch
+        for (uint64_t i = 0; i + 1 < n_ops && i + 1 < cap; ++i)
+            if (p->ops[i].kind == OP_MP && p->ops[i].level == 0 && p->ops[i + 1].kind == OP_LEAF) {
+                out[i + 1].bytes += out[i].bytes;
+                out[i].bytes = 0;
+            }
     }
     *count = n_ops;
     for (auto& e : evs) cudaEventDestroy(e);
