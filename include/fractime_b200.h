@@ -66,7 +66,7 @@ extern "C" {
 /* Scheme ids follow the reference enum SchemeId (schemes.hpp:182):
  * Ode2Sided=0 (here: the one-sided fractional ODE of BASELINE config 1, built
  * from the reference Toeplitz API as in SURVEY.md 3.4), Hyperbolic=1
- * (reference Scheme 2, transport; at most 2048 interior nodes per problem),
+ * (reference Scheme 2, transport),
  * DiffusionWave=2 (reference Scheme 3), Diffusion=3 (Scheme 4). */
 enum {
     FT_SCHEME_ODE = 0,

@@ -42,7 +42,7 @@ class DomainError(FractimeError, ValueError):
 
 class SchemeId(enum.IntEnum):  # reference schemes.hpp:182
     Ode = 0
-    Hyperbolic = 1      # Scheme 2 (transport, 0 < gamma < 1; <= 2048 interior nodes)
+    Hyperbolic = 1      # Scheme 2 (transport, 0 < gamma < 1)
     DiffusionWave = 2
     Diffusion = 3
 

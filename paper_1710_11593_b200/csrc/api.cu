@@ -257,9 +257,14 @@ void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][L][m]*/, do
     const int L = p->L, m = p->slab;
     const double* col = p->col_h.data() + (uint64_t)b * p->N;
     const long double lam = p->lamL[b];
+    // Scheme 2 (stencil): the injection is the left neighbour's boundary value itself
+    // (EL = F before the slab, not lam F): same-step response lam^(q+1), and the history of
+    // the slab's first node also sees that value (B~_j = -A~_j: U_i + U_(i-1))
+    const bool st = p->stencil;
     for (int side = 0; side < 2; ++side) {
         std::vector<std::vector<long double>> g(L, std::vector<long double>(ms));
-        for (int q = 0; q < ms; ++q) g[0][q] = powl(lam, (long double)(side == 0 ? q : ms - 1 - q));
+        for (int q = 0; q < ms; ++q)
+            g[0][q] = powl(lam, (long double)(side == 0 ? q + (st ? 1 : 0) : ms - 1 - q));
         H[0 * 4 + side] = 0.0;
         H[0 * 4 + 2 + side] = 0.0;
         for (int l = 1; l < L; ++l) {
@@ -267,6 +272,10 @@ void slab_responses(const ft_plan* p, int b, int ms, double* G /*[2][L][m]*/, do
             for (int lp = 0; lp < l; ++lp) {
                 const long double c = (uint64_t)(l - lp) < p->N ? (long double)col[l - lp] : 0.0L;
                 for (int q = 0; q < ms; ++q) dr[q] -= c * g[lp][q];
+                if (st) {  // stencil: + the left neighbour of every node (boundary value 1 at lag 0)
+                    for (int q = 1; q < ms; ++q) dr[q] -= c * g[lp][q - 1];
+                    if (lp == 0 && side == 0) dr[0] -= c;
+                }
             }
             long double cF, cB;
             local_solve_ld(p, b, dr, g[l], cF, cB);
@@ -484,7 +493,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     const int slab_min = getenv("FT_SLAB_MIN") ? atoi(getenv("FT_SLAB_MIN")) : 513;
     if (p->kind == SK_DIAG) {
         p->npt = 1; p->L = 32; p->threads = 32; p->slab = 1; p->P = 1;
-    } else if (nodes >= slab_min && !p->stencil) {
+    } else if (nodes >= slab_min) {
         p->npt = 2; p->L = 32; p->threads = 256; p->slab = 512;
         p->P = (nodes + p->slab - 1) / p->slab;
         p->multi = true;
@@ -507,10 +516,6 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         }
     }
     p->P_local = p->P;
-    if (p->stencil && p->multi) {
-        delete p;
-        return set_err(FT_EINVAL, "ft_setup: the hyperbolic scheme supports at most 2048 interior nodes per problem");
-    }
     if (world > 1) {
         if (!p->multi || count != 1 || p->P % world != 0 || rank < 0 || rank >= world) {
             delete p;
@@ -602,6 +607,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             wa.lampow = p->lampow_d;
             wa.lp_stride = p->lp_stride;
             wa.resp_h = p->resph_d;
+            wa.stencil = p->stencil ? 1 : 0;
             FT_CUDA(launch_leaf_wbuild(p->kind, p->L, wa, (int)B, p->respw_d, 0));
             FT_CUDA(cudaDeviceSynchronize());
         }

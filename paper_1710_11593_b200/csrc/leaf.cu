@@ -558,7 +558,7 @@ __device__ __forceinline__ void phase2_rec(const LeafArgs& a, int pb, int len, c
             EL = fma(pc.G0 * lam, FLin, alpha * lamA);
             ER = fma(pc.G0 * lam, BRin, gam * lamB);
         } else {
-            EL = lam * FLin;
+            EL = a.stencil ? FLin : lam * FLin;  // Scheme 2: the boundary value itself (see slab_responses)
             ER = 0.0;
         }
         if (act) out(sl, k, EL, ER);
@@ -764,6 +764,13 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     __syncthreads();
     if (stamp) a.dbg_clk[3] = clock64();
     store_rows<L>(a.X, s_x, rowb, a.N, a.t0, mreal, len, tid, blockDim.x);
+    if (a.V) {  // Scheme 2 product sources V = U_i + U_(i-1); the slab's left neighbour value is EL
+        for (int e = tid; e < mreal * len; e += blockDim.x) {
+            const int q = e / len, k = e - q * len;
+            const double left = q > 0 ? s_x[(q - 1) * (L + 1) + k] : s_inj[k][0];
+            a.V[(rowb + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k] + left;
+        }
+    }
     if (stamp) a.dbg_clk[4] = clock64();
 }
 

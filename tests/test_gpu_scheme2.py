@@ -120,9 +120,16 @@ def test_device_rhs_modes(ft, oracle_mod):
     assert oracle_mod.relerr(Rd.cpu().numpy(), Rh) <= 1e-14
 
 
-def test_rejects_wide_problems(ft):
-    from paper_1710_11593_b200 import InvalidArgument
-
-    w = W.transport(0.5, 64, 4097)
-    with pytest.raises(InvalidArgument, match="2048 interior nodes"):
-        ft.Plan(w.specs)
+@pytest.mark.parametrize("gamma,steps,cells,u0amp", [(0.5, 300, 1100, 1.0),   # 3 slabs, ragged last
+                                                     (0.3, 96, 4097, -0.5),   # 8 slabs (cooperative leaf)
+                                                     (0.8, 64, 2200, None)])
+def test_wide_problems_slab_leaf(ft, oracle_mod, gamma, steps, cells, u0amp):
+    """Problems wider than 512 nodes: the slab (SPIKE) leaf with the stencil-aware
+    response tables (the injection is the left neighbour's boundary value, which also
+    enters the first node's history) and V written from the corrected tile."""
+    w = W.transport(gamma, steps, cells, u0amp)
+    F, u0 = _inputs(oracle_mod, w)
+    plan = ft.Plan(w.specs)
+    assert plan.info.slabs > 1
+    U, _ = plan.solve_fast(plan.assemble_rhs_grid(F, u0))
+    assert oracle_mod.relerr(U, oracle_mod.direct(w, F, u0)) <= TOL

@@ -103,12 +103,15 @@ class _LocalExchange:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,cells,steps", [(2, 4097, 200), (4, 4097, 96), (2, 65537, 64)])
-def test_sharded_plan_matches_single(ft, oracle_mod, world, cells, steps):
-    w = W.config(4, time_steps=steps, cells=cells)
+@pytest.mark.parametrize("world,cells,steps,scheme", [(2, 4097, 200, 4), (4, 4097, 96, 4), (2, 65537, 64, 4),
+                                                      (2, 2049, 128, 2), (4, 2049, 70, 2)])
+def test_sharded_plan_matches_single(ft, oracle_mod, world, cells, steps, scheme):
+    """scheme 4: config 4 shapes; scheme 2: transport (stencil history across the rank boundary)."""
+    w = W.config(4, time_steps=steps, cells=cells) if scheme == 4 else W.transport(0.4, steps, cells, 1.0)
     F = oracle_mod.forcing_grid(w)
+    u0 = oracle_mod.initial_grid(w, w.u0amp)
     single = ft.Plan(w.specs)
-    R = single.assemble_rhs_grid(F)
+    R = single.assemble_rhs_grid(F, u0)
     U1, _ = single.solve_fast(R)
     ex = _LocalExchange(world)
     plans = [par.ShardedPlan(w.specs[0], r, world, exchange_factory=ex.factory(r)) for r in range(world)]
@@ -133,4 +136,4 @@ def test_sharded_plan_matches_single(ft, oracle_mod, world, cells, steps):
     U = np.vstack(outs)
     assert np.array_equal(U, U1)
     if cells <= 4097:
-        assert oracle_mod.relerr(U, oracle_mod.direct(w, F)) <= 1e-10
+        assert oracle_mod.relerr(U, oracle_mod.direct(w, F, u0)) <= 1e-10
