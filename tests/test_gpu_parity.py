@@ -246,19 +246,23 @@ def test_streamed_host_solve(ft, oracle_mod, cid, kw):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference")])
+@pytest.mark.parametrize("eid,key", [(4, "kDiffusionReference"), (3, "kWaveReference"),
+                                     (2, "kTransportReference")])
 def test_harness_convergence_tables(ft, eid, key):
     """The GPU harness (device RHS, fast D&C) reproduces the reference's frozen
-    convergence tables (acceptance.cpp:206-255) in the reference CSV format."""
+    convergence tables (acceptance.cpp:206-255) in the reference CSV format
+    (Example 2 at tau = 2^-10 and one tenth of its frozen column: the reference's
+    documented x10 defect, proj/README.md:92-96)."""
     import json
     from pathlib import Path
 
     from paper_1710_11593_b200 import harness as H
 
     col = json.loads((Path(__file__).resolve().parent / "golden" / "tables.json").read_text())[key][1]
-    rows = H.run_convergence(eid, [col["gamma"]], H.exponent_ladder(3, 8))
+    scale = 0.1 if eid == 2 else 1.0
+    rows = H.run_convergence(eid, [col["gamma"]], H.exponent_ladder(3, 8, 10 if eid == 2 else None))
     for r, err in zip(rows, col["errors"]):
-        assert abs(r.l2_error - err) <= 0.05 * err
+        assert abs(r.l2_error - scale * err) <= 0.05 * scale * err
     for r, rate in zip(rows[1:], col["rates"]):
         assert abs(r.rate - rate) <= 0.05
     csv = H.emit_csv(rows).splitlines()
