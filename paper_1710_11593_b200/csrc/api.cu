@@ -819,6 +819,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.pair_begin = 0;
             a.pair_count = 0;
             FT_CUDA(launch_mp(a, lv.groups, st));
+            nl += mp_kernel_count(a) - 1;  // split levels launch several kernels per product
         }
         ++nl;
     }

@@ -212,6 +212,7 @@ constexpr uint64_t kMpScratchBytes = 256ull << 20;  // split K-branch scratch (L
 cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, int J, cplx* spec,
                                   const cplx* tw, cudaStream_t st);
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st);
+int mp_kernel_count(const MpArgs& a);
 cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
                            cplx* spec, const cplx* tw, int logT, cudaStream_t st);
 cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a, int ctas,

@@ -1058,6 +1058,16 @@ cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, i
     return cudaErrorInvalidValue;
 }
 
+// Kernels launch_mp issues for this product (split levels: 2 or 3 per pair batch).
+int mp_kernel_count(const MpArgs& a) {
+    if (mp_is_single(a.n) || mp_is_direct(a.n) || !a.scratch) return 1;
+    static const int prefold_min_k = getenv("FT_PREFOLD_MIN_K") ? atoi(getenv("FT_PREFOLD_MIN_K")) : 16;
+    const bool prefold = a.K >= prefold_min_k && getenv("FT_NO_PREFOLD") == nullptr;
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const int batch = (int)std::max<uint64_t>(1, split_batch_bytes() / ((uint64_t)a.K * a.m * sizeof(cplx)));
+    return ((npairs + batch - 1) / batch) * (prefold ? 3 : 2);
+}
+
 cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
     if (mp_is_single(a.n)) {
         switch (a.n) {
