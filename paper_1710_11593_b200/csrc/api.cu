@@ -1413,6 +1413,7 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
     ra.wts = p->wts_d;
     ra.cvals = c_d;
     const int J = std::max(1, gen_terms(ra));
+    if (J > 16) return set_err(FT_EINVAL, "ft_solve_fast_modes: at most 14 forcing modes");
     const size_t ab = sizeof(double) * rows_of(p) * J, tb = sizeof(double) * (size_t)B * p->N * J;
     if (ab != p->genA_bytes) {
         if (p->genA_d) cudaFree(p->genA_d);

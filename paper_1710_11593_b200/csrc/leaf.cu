@@ -348,6 +348,13 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         // straight into the register window; T is warp-uniform (broadcast loads)
         const int J = a.genJ;
         const double* Tb = a.genT + ((uint64_t)pb * N + a.t0) * J;
+        constexpr int kMaxJ = 16;
+        __shared__ double s_T[kMaxJ][L];  // this leaf's step factors, [j][k] (broadcast reads)
+        for (int e = tid; e < kMaxJ * L; e += blockDim.x) {
+            const int j = e / L, k = e - j * L;
+            s_T[j][k] = (j < J && k < len) ? __ldg(&Tb[(uint64_t)k * J + j]) : 0.0;
+        }
+        __syncthreads();
 #pragma unroll 1
         for (int j = 0; j < J; ++j) {
             double av[NPT];
@@ -357,10 +364,13 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
                 av[v] = q < mreal ? __ldg(&a.genA[(rowb + q) * J + j]) : 0.0;
             }
 #pragma unroll
-            for (int k = 0; k < L; ++k) {
-                const double t = k < len ? __ldg(&Tb[(uint64_t)k * J + j]) : 0.0;
+            for (int k = 0; k < L; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(&s_T[j][k]);
 #pragma unroll
-                for (int v = 0; v < NPT; ++v) tile[v][k] = fma(av[v], t, tile[v][k]);
+                for (int v = 0; v < NPT; ++v) {
+                    tile[v][k] = fma(av[v], t2.x, tile[v][k]);
+                    tile[v][k + 1] = fma(av[v], t2.y, tile[v][k + 1]);
+                }
             }
         }
     }
