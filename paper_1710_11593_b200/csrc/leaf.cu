@@ -329,16 +329,24 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
                 double u[L];
 #pragma unroll
                 for (int jj = 0; jj < L; ++jj) u[jj] = s_out[q * (L + 1) + jj];
+                // 8 outputs at a time: each output still sums jj ascending (bitwise equal to
+                // the standalone direct product) with 8 independent FMA chains in flight
 #pragma unroll
-                for (int k = 0; k < L; ++k) {
-                    double acc = 0.0;
+                for (int k0 = 0; k0 < L; k0 += 8) {
+                    double acc[8];
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
 #pragma unroll
                     for (int jj = 0; jj < L; ++jj) {
-                        const int lag = L + k - jj;  // 1 .. 2L-1
-                        const double c = lag < L ? a.kc[lag] : a.kc[kKcCol2 + lag - L];
-                        acc = fma(c, u[jj], acc);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const int lag = L + k0 + kk - jj;  // 1 .. 2L-1
+                            const double c = lag < L ? a.kc[lag] : a.kc[kKcCol2 + lag - L];
+                            acc[kk] = fma(c, u[jj], acc[kk]);
+                        }
                     }
-                    tile[v][k] -= acc;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) tile[v][k0 + kk] -= acc[kk];
                 }
             }
         }
