@@ -102,18 +102,21 @@ template <int NPT, int L>
 struct LeafConsts<true, NPT, L> {
     const LeafArgs& a;
     double lamLaneF, lamLaneB;
+    double pwF[5], pwB[5];  // lane-masked shuffle-scan multipliers (0 where the partner is out of range):
+                            // one DFMA per round instead of DFMA + two selects
     __device__ __forceinline__ LeafConsts(const LeafArgs& a_, int, const double* lp, double, int lane) : a(a_) {
         lamLaneF = lp[min(NPT * lane, a.lp_stride - 1)];
         lamLaneB = lp[min(NPT * (31 - lane), a.lp_stride - 1)];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            pwF[d] = lane >= (1 << d) ? a.kc[kKcPow + d] : 0.0;
+            pwB[d] = lane + (1 << d) < 32 ? a.kc[kKcPow + d] : 0.0;
+        }
     }
     __device__ __forceinline__ double cw(int j) const { return a.kc[j]; }
     __device__ __forceinline__ double lam() const { return a.kc[kKcLam]; }
-    __device__ __forceinline__ double stepF(int d, double y, double S, int lane) const {
-        return lane >= (1 << d) ? fma(a.kc[kKcPow + d], y, S) : S;
-    }
-    __device__ __forceinline__ double stepB(int d, double y, double S, int lane) const {
-        return lane + (1 << d) < 32 ? fma(a.kc[kKcPow + d], y, S) : S;
-    }
+    __device__ __forceinline__ double stepF(int d, double y, double S, int) const { return fma(pwF[d], y, S); }
+    __device__ __forceinline__ double stepB(int d, double y, double S, int) const { return fma(pwB[d], y, S); }
     __device__ __forceinline__ double exF(double y, int lane) const { return lane > 0 ? y : 0.0; }
     __device__ __forceinline__ double exB(double y, int lane) const { return lane < 31 ? y : 0.0; }
     __device__ __forceinline__ double lamW() const { return a.kc[kKcLamW]; }
