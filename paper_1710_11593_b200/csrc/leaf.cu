@@ -445,24 +445,26 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         }
 #pragma unroll
         for (int v = 0; v < NPT; ++v) {
-            x[v] *= vmask[v];  // padding nodes stay exactly zero
+            if (padded) x[v] *= vmask[v];  // padding nodes stay exactly zero
             outp[v * (L + 1)] = x[v];
         }
+        // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
+        double xs[NPT];
 #pragma unroll
-        for (int v = NPT - 1; v >= 0; --v) {
-            // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
-            const double xs = a.stencil ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
-            // push x_k into the remaining in-leaf steps; chunks whose first entry lies
-            // past the leaf end (k + 1 + c >= len) are dead and skipped (warp-uniform)
+        for (int v = 0; v < NPT; ++v) xs[v] = a.stencil ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
+        // push x_k into the remaining in-leaf steps; chunks whose first entry lies past
+        // the leaf end (k + 1 + c >= len) are dead and skipped (one warp-uniform test per chunk)
 #pragma unroll
-            for (int c = 0; c + 1 < L; c += 8) {
-                if (c == 0 || k + 1 + c < len) {
+        for (int c = 0; c + 1 < L; c += 8) {
+            if (c == 0 || k + 1 + c < len) {
 #pragma unroll
-                    for (int i = c; i < c + 8 && i + 1 < L; ++i) tile[v][i] = fma(-sc.cw(i + 1), xs, tile[v][i + 1]);
-                }
+                for (int v = 0; v < NPT; ++v)
+#pragma unroll
+                    for (int i = c; i < c + 8 && i + 1 < L; ++i) tile[v][i] = fma(-sc.cw(i + 1), xs[v], tile[v][i + 1]);
             }
-            tile[v][L - 1] = 0.0;
         }
+#pragma unroll
+        for (int v = 0; v < NPT; ++v) tile[v][L - 1] = 0.0;
         ++outp;
     }
 
