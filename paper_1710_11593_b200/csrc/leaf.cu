@@ -219,17 +219,19 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
     constexpr int nw = kLeafThreads / 32;
     constexpr bool TRI = KIND == SK_TRIDIAG;
     double f[NPT], bl[NPT];
-    double acc = 0.0;
+    double acc = in[0];  // (no 0 * lam + in on the step's critical path)
+    f[0] = acc;
 #pragma unroll
-    for (int v = 0; v < NPT; ++v) {
+    for (int v = 1; v < NPT; ++v) {
         acc = fma(sc.lam(), acc, in[v]);
         f[v] = acc;
     }
     double SF = acc, SB = 0.0;
     if (TRI) {
-        double accb = 0.0;
+        double accb = in[NPT - 1];
+        bl[NPT - 1] = accb;
 #pragma unroll
-        for (int v = NPT - 1; v >= 0; --v) {
+        for (int v = NPT - 2; v >= 0; --v) {
             accb = fma(sc.lam(), accb, in[v]);
             bl[v] = accb;
         }
@@ -451,7 +453,8 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
         double xs[NPT];
 #pragma unroll
-        for (int v = 0; v < NPT; ++v) xs[v] = a.stencil ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
+        for (int v = 0; v < NPT; ++v)  // (compile-time false for the tridiagonal operator: x stays on the fast path)
+            xs[v] = (KIND == SK_UPWIND && a.stencil) ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
         // push x_k into the remaining in-leaf steps; chunks whose first entry lies past
         // the leaf end (k + 1 + c >= len) are dead and skipped (one warp-uniform test per chunk)
 #pragma unroll
