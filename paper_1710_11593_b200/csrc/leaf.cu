@@ -212,7 +212,12 @@ __device__ __forceinline__ void store_rows(double* X, const double* src, uint64_
 // Forward (and, for TRIDIAG, backward) lam-decay scans over the CTA's nodes
 // with zero carry in at both ends.  Fv/Bv: scans at this thread's nodes;
 // totF: F at the CTA's last (possibly padding) node; totB: B at its first.
-template <int KIND, int NPT, class SC>
+// FULL = true: every thread gets totF / totB (single-CTA mode, Dirichlet
+// correction).  FULL = false (slab mode): warp w chains only the warp totals it
+// needs, as warp-uniform predicated DFMAs (same order, so bitwise the same
+// carries; no selects): totF is the CTA total in the last warp, totB in warp 0
+// -- their only consumers are the exported slab carries.
+template <int KIND, int NPT, bool FULL, class SC>
 __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
                                          double (*s_wt)[2], int lane, int w, double (&Fv)[NPT],
                                          double (&Bv)[NPT], double& totF, double& totB, double& Fpv) {
@@ -252,19 +257,33 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
     if (lane == 0) s_wt[w][1] = SB;
     __syncthreads();
     // cross-warp carries: short sequential chains over the 8 warp totals
-    double CF = 0.0, runF = 0.0, CB = 0.0, runB = 0.0;
+    double CF = 0.0, CB = 0.0;
+    if constexpr (FULL) {
+        double runF = 0.0, runB = 0.0;
 #pragma unroll
-    for (int ww = 0; ww < nw; ++ww) {
-        if (ww == w) CF = runF;
-        runF = fma(sc.lamW(), runF, s_wt[ww][0]);
-        if (TRI) {
-            const int wb = nw - 1 - ww;
-            if (wb == w) CB = runB;
-            runB = fma(sc.lamW(), runB, s_wt[wb][1]);
+        for (int ww = 0; ww < nw; ++ww) {
+            if (ww == w) CF = runF;
+            runF = fma(sc.lamW(), runF, s_wt[ww][0]);
+            if (TRI) {
+                const int wb = nw - 1 - ww;
+                if (wb == w) CB = runB;
+                runB = fma(sc.lamW(), runB, s_wt[wb][1]);
+            }
         }
+        totF = runF;
+        totB = runB;
+    } else {
+#pragma unroll
+        for (int ww = 0; ww < nw; ++ww)
+            if (ww < w) CF = fma(sc.lamW(), CF, s_wt[ww][0]);
+        if (TRI) {
+#pragma unroll
+            for (int wb = nw - 1; wb >= 0; --wb)
+                if (wb > w) CB = fma(sc.lamW(), CB, s_wt[wb][1]);
+        }
+        totF = fma(sc.lamW(), CF, s_wt[w][0]);
+        totB = TRI ? fma(sc.lamW(), CB, s_wt[w][1]) : 0.0;
     }
-    totF = runF;
-    totB = runB;
     const double Fprev = fma(sc.laneF(), CF, exF);
     Fpv = Fprev;  // F at the node before this thread's first node (0 before node 0)
 #pragma unroll
@@ -420,7 +439,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 #pragma unroll
             for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] / pc.d : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
-            cta_scan<KIND, NPT>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB, xleft);
+            cta_scan<KIND, NPT, MODE == 0>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB, xleft);
             double cF = totF;
             if (padded) {  // F at the last real node (padding nodes carry zeros)
                 if (tid == own_t) {
@@ -431,9 +450,9 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
                 __syncthreads();
                 cF = s_own[par];
             }
-            if (MODE == 1 && tid == 0) {
-                s_cx[k][0] = cF;
-                s_cx[k][1] = totB;
+            if (MODE == 1) {  // exported carries: F at the slab's last node, B at its first
+                if (padded ? tid == 0 : (w == kLeafThreads / 32 - 1 && lane == 31)) s_cx[k][0] = cF;
+                if (tid == 0) s_cx[k][1] = totB;
             }
 #pragma unroll
             for (int v = 0; v < NPT; ++v) {
