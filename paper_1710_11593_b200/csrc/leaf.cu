@@ -23,6 +23,9 @@
 //     space-time response tables GL, GR: x += sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l).
 #include "internal.cuh"
 
+#ifndef FT_LEAF_WREG
+#define FT_LEAF_WREG 0  // 1: batched plans copy the in-leaf weights into registers (old path)
+#endif
 #ifndef FT_LEAF_UNROLL
 #define FT_LEAF_UNROLL 1  // step-loop unroll: 1 measured 403 ms vs 408 (2) and 412 (4) on cfg4 (instruction fetch)
 #endif
@@ -78,12 +81,21 @@ struct LeafConsts;
 template <int NPT, int L>
 struct LeafConsts<false, NPT, L> {
     ScanConsts<NPT> sc;
+#if FT_LEAF_WREG
     double w[L];
+#else
+    const double* w;  // this problem's row of c_leafcol: read per use through the constant cache
+                      // (CTA-uniform index; 31 weights in registers spilled)
+#endif
     __device__ __forceinline__ LeafConsts(const LeafArgs& a, int pb, const double* lp, double lam, int lane) {
         scan_consts<NPT>(sc, lp, a.lp_stride, lam, lane);
         const double* cc = c_leafcol[pb < kMaxLeafProblems ? pb : 0];
+#if FT_LEAF_WREG
 #pragma unroll
         for (int j = 0; j < L; ++j) w[j] = cc[j];
+#else
+        w = cc;
+#endif
     }
     __device__ __forceinline__ double cw(int j) const { return w[j]; }
     __device__ __forceinline__ double lam() const { return sc.lam; }
