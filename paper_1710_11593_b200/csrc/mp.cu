@@ -785,13 +785,18 @@ __global__ void __launch_bounds__(kMpThreads, 1) spec1_kernel(const double* col,
 // Each thread owns 16 consecutive outputs of one row; a warp spans 32 rows
 // with the same outputs so the column window is warp-uniform (SMEM
 // broadcast), and the 16x16 block products are fully unrolled on registers.
+#ifndef FT_DIR_THREADS
+#define FT_DIR_THREADS 128  // 4 CTAs of 4 warps per SM: config 5 92.0 -> 91.5 ms (n = 128 level 6.3 -> 5.8), config 4 neutral; 512 slower
+#endif
+constexpr int kDirThreads = FT_DIR_THREADS;  // threads per direct-product CTA
+
 template <int H>
-__global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
+__global__ void __launch_bounds__(kDirThreads, 512 / kDirThreads) mp_direct_kernel(MpArgs a) {
     pdl_launch_dependents(a.pdl_trigger);
     pdl_wait();
     constexpr int TT = H < 16 ? H : 16;
     constexpr int TPR = H / TT;                      // threads per row
-    constexpr int RPC = kMpThreads / TPR;            // rows per CTA
+    constexpr int RPC = kDirThreads / TPR;            // rows per CTA
     constexpr int LD = H + 1;                        // padded row stride (conflict-free)
     __shared__ double s_c[2 * H + TT];
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -807,11 +812,11 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
     for (int k = tid; k < 2 * H + TT; k += blockDim.x) s_c[k] = (k >= 1 && k < 2 * H && (uint64_t)k < N) ? colp[k] : 0.0;
     // coalesced staging: a warp reads 32 consecutive time steps of one row; all
     // of a thread's loads are issued before any store (memory-level parallelism)
-    constexpr int PER = RPC * H / kMpThreads;  // 16
+    constexpr int PER = RPC * H / kDirThreads;  // 16
     double uu[PER], rv[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-        const int e = tid + i * kMpThreads;
+        const int e = tid + i * kDirThreads;
         const int r2 = e / H, j = e - r2 * H;
         const uint64_t row = row0 + r2;
         const bool ok = row < (uint64_t)a.rows;
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_direct_kernel(MpArgs a) {
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-        const int e = tid + i * kMpThreads;
+        const int e = tid + i * kDirThreads;
         const int r2 = e / H, j = e - r2 * H;
         s_u[r2 * LD + j] = uu[i];
         s_r[r2 * LD + j] = rv[i];
@@ -985,7 +990,7 @@ static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
 
 template <int H>
 static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
-    constexpr int RPC = kMpThreads / (H / (H < 16 ? H : 16));
+    constexpr int RPC = kDirThreads / (H / (H < 16 ? H : 16));
     const size_t smem = sizeof(double) * 2 * RPC * (H + 1);
     static bool attr_set = false;
     if (!attr_set) {
@@ -993,7 +998,7 @@ static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
         attr_set = true;
     }
     const int ctas = (a.rows + RPC - 1) / RPC;
-    return launch_ex(mp_direct_kernel<H>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
+    return launch_ex(mp_direct_kernel<H>, dim3(ctas), dim3(kDirThreads), smem, st, 1, a);
 }
 
 bool mp_is_direct(int n) { return n <= 2 * kMpDirectMaxH; }
