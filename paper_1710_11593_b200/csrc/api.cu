@@ -1236,6 +1236,13 @@ static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* r
 // rank; keyed by the buffers and the fused-RHS tables), else launched directly.
 static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* gen, uint64_t* launches) {
     const cudaStream_t st = p->stream;
+    // single-node (ODE) problems: the whole time march in one kernel per call
+    static const bool no_ode1 = getenv("FT_NO_ODE1") != nullptr;  // A/B switch: the D&C schedule instead
+    if (!gen && !no_ode1 && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N)) {
+        FT_CUDA(launch_ode_whole(X, src, p->col_d, p->pc_d, p->N, p->B, st));
+        *launches = 1;
+        return FT_OK;
+    }
     const bool use_graph = (p->part_world == 1 || p->p2p) && !getenv("FT_NO_GRAPH");
     if (!use_graph) return run_fast(p, X, src, launches, nullptr, nullptr, gen);
     const void* gkey = gen ? (const void*)gen->A : nullptr;

@@ -205,3 +205,140 @@ cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st) {
 }
 
 }  // namespace ftb
+
+namespace ftb {
+
+// ---- whole fast solve of single-node (ODE) problems: one CTA per problem ----
+// u[n] = (r[n] - sum_{j<n} col[n-j] u[j]) / col[0]  (the reference's one-sided ODE
+// march, fractional_ode.cpp via SURVEY 8a; same equations as the D&C leaf with
+// nodes = 1).  Such a problem is one time row: the D&C's ~2N/32 launches are pure
+// latency, so the CTA keeps the solved prefix of u in shared memory and walks
+// 32-step blocks: while warp 0 solves block b (its 32 dependent steps by
+// shuffles), 12 warps form block b+1's history sum_{j<t0} col[t0+32+k-j] u[j]
+// over the steps solved before block b (register-blocked Toeplitz products).
+#ifndef FT_ODE_NOHIST
+#define FT_ODE_NOHIST 0  // timing probes only (wrong results)
+#endif
+#ifndef FT_ODE_NOSEQ
+#define FT_ODE_NOSEQ 0
+#endif
+#ifndef FT_ODE_DIV
+#define FT_ODE_DIV 0
+#endif
+constexpr int kOdeSets = 3;                       // history warp sets (4 warps each: 8 outputs per warp)
+constexpr int kOdeThreads = 32 * (1 + 4 * kOdeSets);
+#ifndef FT_ODE_CHAINS
+#define FT_ODE_CHAINS 8
+#endif
+constexpr int kOdeChains = FT_ODE_CHAINS;  // independent partial sums per lane (loads in flight)
+
+__global__ void __launch_bounds__(kOdeThreads, 1) ode_whole_kernel(double* X, const double* R, const double* col,
+                                                                   const ProblemConst* pcs, uint64_t N) {
+    extern __shared__ __align__(16) double s_u[];  // [N] solved steps
+    __shared__ double s_hp[2][kOdeSets][32];       // next block's history, per warp set (double-buffered)
+    __shared__ double s_c[64];                     // col[0..64)
+    const int pb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const double* c = col + (uint64_t)pb * N;
+    const double* r = R + (uint64_t)pb * N;
+    double* x = X + (uint64_t)pb * N;
+    const double d = pcs[pb].d, dinv = 1.0 / d;
+    (void)d;
+    (void)dinv;
+    if (tid < 64) s_c[tid] = (uint64_t)tid < N ? c[tid] : 0.0;
+    double rnext = lane < N ? r[lane] : 0.0;  // (warp 0: block 0's R)
+    for (int i = tid; i < kOdeSets * 32; i += blockDim.x) (&s_hp[0][0][0])[i] = 0.0;
+    __syncthreads();
+    const uint64_t nb = (N + 31) / 32;
+    for (uint64_t b = 0; b < nb; ++b) {
+        const uint64_t t0 = b * 32;
+        const int len = (int)(N - t0 < 32 ? N - t0 : 32);
+        const int cur = (int)(b & 1);
+        if (w == 0) {
+            // block b: its history over steps < t0 - 32 is in s_hp[cur]; add the previous
+            // block's 32 steps (u just solved) here, then the 32 dependent steps
+            const double rcur = rnext;
+            if (t0 + 32 + lane < N) rnext = r[t0 + 32 + lane];  // next block's R: in flight during this one
+            double hk = 0.0;
+#pragma unroll
+            for (int q = 0; q < kOdeSets; ++q) hk += s_hp[cur][q][lane];
+            double rk = lane < len ? rcur - hk : 0.0;
+            if (b > 0 && lane < len) {
+                const uint64_t p0 = t0 - 32;
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j & 3] = fma(s_c[32 + lane - j], s_u[p0 + j], acc[j & 3]);
+                rk -= (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            }
+            double ux = 0.0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i >= len || FT_ODE_NOSEQ) break;
+#if FT_ODE_DIV
+                const double xi = __shfl_sync(0xffffffffu, rk, i) / d;
+#else
+                const double xi = __shfl_sync(0xffffffffu, rk, i) * dinv;  // (a division is ~10x the latency)
+#endif
+                if (lane == i) ux = xi;
+                if (lane > i) rk = fma(-s_c[lane - i], xi, rk);
+            }
+            if (lane < len) {
+                s_u[t0 + lane] = ux;
+                x[t0 + lane] = ux;
+            }
+        } else if (b + 1 < nb && !FT_ODE_NOHIST) {
+            // next block's history over steps < t0 (all solved before this block):
+            // warp (set, g) covers outputs k in [8g, 8g+8); each lane a slice of the
+            // j range, with a sliding column window (8 FMA per 2 loads), then a
+            // reduction over the warp's slices; warp 0 adds the kOdeSets partials
+            const int hw = w - 1, g = hw & 3, set = hw >> 2;
+            const int sl = set * 32 + lane;
+            constexpr int NS = kOdeSets * 32;
+            const uint64_t per = (t0 + NS - 1) / NS;
+            const uint64_t j0 = min(t0, (uint64_t)sl * per), j1 = min(t0, j0 + per);
+            const uint64_t kb = t0 + 32 + 8 * g;  // column index of output 8g at step j is kb - j
+            double acc[8], cw[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                acc[i] = 0.0;
+                cw[i] = (j0 < j1 && kb + i - j0 < N) ? __ldg(c + (kb + i - j0)) : 0.0;
+            }
+            for (uint64_t j = j0; j < j1; ++j) {
+                const double uj = s_u[j];
+                const uint64_t nx = kb - j - 1;  // next step's window entry 0 (>= 32)
+                const double cn = nx < N ? __ldg(c + nx) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = fma(cw[i], uj, acc[i]);
+#pragma unroll
+                for (int i = 7; i > 0; --i) cw[i] = cw[i - 1];
+                cw[0] = cn;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+            double v = acc[0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) v = lane == i ? acc[i] : v;
+            if (lane < 8) s_hp[cur ^ 1][set][8 * g + lane] = v;
+        }
+        __syncthreads();
+    }
+}
+
+bool ode_whole_ok(uint64_t N) { return N >= 1 && N * sizeof(double) <= 200 * 1024; }
+
+cudaError_t launch_ode_whole(double* X, const double* R, const double* col, const ProblemConst* pc, uint64_t N,
+                             int B, cudaStream_t st) {
+    const size_t smem = N * sizeof(double);
+    static size_t set = 0;
+    if (smem > 48 * 1024 && smem > set) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(ode_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        set = smem;
+    }
+    ode_whole_kernel<<<B, kOdeThreads, smem, st>>>(X, R, col, pc, N);
+    return cudaGetLastError();
+}
+
+}  // namespace ftb

@@ -226,6 +226,9 @@ cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st);
 // buffers [2 parities][P][L][2] doubles
 constexpr size_t kP2pHeader = 64;
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
+bool ode_whole_ok(uint64_t N);
+cudaError_t launch_ode_whole(double* X, const double* R, const double* col, const ProblemConst* pc, uint64_t N,
+                             int B, cudaStream_t st);
 cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
 int gen_terms(const RhsModesArgs& a);  // J of the separable RHS tables

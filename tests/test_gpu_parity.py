@@ -353,3 +353,24 @@ def test_edge_shapes(ft, oracle_mod, cid, kw):
     ref = oracle_mod.direct(w, F, u0, phi)
     _, _, U, _ = _fast(ft, w, F, u0, phi)
     assert oracle_mod.relerr(U, ref) <= TOL
+
+
+@pytest.mark.parametrize("steps", [1, 32, 33, 40, 1000, 4096, 25600, 25601])
+def test_ode_whole_march(ft, oracle_mod, steps):
+    """Single-node (ODE) problems solve in one kernel per call (one CTA per problem,
+    the solved prefix in shared memory; up to 25600 steps), batched problems with
+    different orders; longer ones keep the D&C schedule.  Both against the oracle."""
+    from paper_1710_11593_b200 import ProblemSpec, SchemeId
+    gammas = [0.3, 0.5, 0.8] if steps <= 4096 else [0.5]
+    specs = [ProblemSpec(SchemeId.Ode, g, steps, 0, steps / 4096, 1.0) for g in gammas]
+    B = len(specs)
+    import math
+    a = np.array([[2.0 / math.gamma(3.0 - g), 1.0, 1.0] for g in gammas])
+    p = np.array([[2.0 - g, 2.0, 0.0] for g in gammas])
+    w = W.Workload("ode-batch", specs, a, np.array([1.0, 1.0, 1.0]), p, np.array([2, 2, 2]),
+                   np.ones(B), None, "t^2+1")
+    F, u0, phi = _inputs(oracle_mod, w)
+    ref = oracle_mod.direct(w, F, u0, phi)
+    _, _, U, rep = _fast(ft, w, F, u0, phi)
+    assert oracle_mod.relerr(U, ref) <= TOL
+    assert (rep.kernel_launches == 1) == (steps <= 25600)
