@@ -232,9 +232,11 @@ constexpr int kOdeThreads = 32 * (1 + 4 * kOdeSets);
 #endif
 constexpr int kOdeChains = FT_ODE_CHAINS;  // independent partial sums per lane (loads in flight)
 
+template <bool SC>  // SC: the column is staged in shared memory too (16 N bytes fit)
 __global__ void __launch_bounds__(kOdeThreads, 1) ode_whole_kernel(double* X, const double* R, const double* col,
                                                                    const ProblemConst* pcs, uint64_t N) {
-    extern __shared__ __align__(16) double s_u[];  // [N] solved steps
+    extern __shared__ __align__(16) double s_u[];  // [N] solved steps, then (SC) [N] column
+    double* s_col = s_u + N;
     __shared__ double s_hp[2][kOdeSets][32];       // next block's history, per warp set (double-buffered)
     __shared__ double s_c[64];                     // col[0..64)
     const int pb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -247,6 +249,9 @@ __global__ void __launch_bounds__(kOdeThreads, 1) ode_whole_kernel(double* X, co
     if (tid < 64) s_c[tid] = (uint64_t)tid < N ? c[tid] : 0.0;
     double rnext = lane < N ? r[lane] : 0.0;  // (warp 0: block 0's R)
     for (int i = tid; i < kOdeSets * 32; i += blockDim.x) (&s_hp[0][0][0])[i] = 0.0;
+    if (SC)
+        for (uint64_t i = tid; i < N; i += blockDim.x) s_col[i] = __ldg(c + i);
+    auto colv = [&](uint64_t i) { return SC ? s_col[i] : __ldg(c + i); };
     __syncthreads();
     const uint64_t nb = (N + 31) / 32;
     for (uint64_t b = 0; b < nb; ++b) {
@@ -293,19 +298,19 @@ __global__ void __launch_bounds__(kOdeThreads, 1) ode_whole_kernel(double* X, co
             const int hw = w - 1, g = hw & 3, set = hw >> 2;
             const int sl = set * 32 + lane;
             constexpr int NS = kOdeSets * 32;
-            const uint64_t per = (t0 + NS - 1) / NS;
+            const uint64_t per = ((t0 + NS - 1) / NS) | 1;  // odd slice stride: spread over the banks
             const uint64_t j0 = min(t0, (uint64_t)sl * per), j1 = min(t0, j0 + per);
             const uint64_t kb = t0 + 32 + 8 * g;  // column index of output 8g at step j is kb - j
             double acc[8], cw[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 acc[i] = 0.0;
-                cw[i] = (j0 < j1 && kb + i - j0 < N) ? __ldg(c + (kb + i - j0)) : 0.0;
+                cw[i] = (j0 < j1 && kb + i - j0 < N) ? colv(kb + i - j0) : 0.0;
             }
             for (uint64_t j = j0; j < j1; ++j) {
                 const double uj = s_u[j];
                 const uint64_t nx = kb - j - 1;  // next step's window entry 0 (>= 32)
-                const double cn = nx < N ? __ldg(c + nx) : 0.0;
+                const double cn = nx < N ? colv(nx) : 0.0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) acc[i] = fma(cw[i], uj, acc[i]);
 #pragma unroll
@@ -325,19 +330,25 @@ __global__ void __launch_bounds__(kOdeThreads, 1) ode_whole_kernel(double* X, co
     }
 }
 
-bool ode_whole_ok(uint64_t N) { return N >= 1 && N * sizeof(double) <= 200 * 1024; }
+constexpr uint64_t kOdeSmem = 200 * 1024;
+bool ode_whole_ok(uint64_t N) { return N >= 1 && N * sizeof(double) <= kOdeSmem; }
 
 cudaError_t launch_ode_whole(double* X, const double* R, const double* col, const ProblemConst* pc, uint64_t N,
                              int B, cudaStream_t st) {
-    const size_t smem = N * sizeof(double);
-    static size_t set = 0;
-    if (smem > 48 * 1024 && smem > set) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(ode_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool sc = 2 * N * sizeof(double) <= kOdeSmem;
+    const size_t smem = (sc ? 2 : 1) * N * sizeof(double);
+    static bool set = false;
+    if (!set) {
+        cudaError_t e = cudaFuncSetAttribute(ode_whole_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOdeSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ode_whole_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOdeSmem);
         if (e != cudaSuccess) return e;
-        set = smem;
+        set = true;
     }
-    ode_whole_kernel<<<B, kOdeThreads, smem, st>>>(X, R, col, pc, N);
+    if (sc)
+        ode_whole_kernel<true><<<B, kOdeThreads, smem, st>>>(X, R, col, pc, N);
+    else
+        ode_whole_kernel<false><<<B, kOdeThreads, smem, st>>>(X, R, col, pc, N);
     return cudaGetLastError();
 }
 

@@ -355,7 +355,7 @@ def test_edge_shapes(ft, oracle_mod, cid, kw):
     assert oracle_mod.relerr(U, ref) <= TOL
 
 
-@pytest.mark.parametrize("steps", [1, 32, 33, 40, 1000, 4096, 25600, 25601])
+@pytest.mark.parametrize("steps", [1, 32, 33, 40, 1000, 4096, 12800, 12801, 25600, 25601])
 def test_ode_whole_march(ft, oracle_mod, steps):
     """Single-node (ODE) problems solve in one kernel per call (one CTA per problem,
     the solved prefix in shared memory; up to 25600 steps), batched problems with
