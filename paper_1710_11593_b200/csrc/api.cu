@@ -133,6 +133,7 @@ struct ft_plan {
     size_t genA_bytes = 0, genT_bytes = 0;
     double* genArgs_d = nullptr;  // ft_solve_fast_modes argument block
     size_t genArgs_bytes = 0;
+    double* oder_d = nullptr;     // ft_solve_fast_modes on single-node plans: the RHS array
     uint64_t graph_launches = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -1421,6 +1422,37 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
     ra.cvals = c_d;
     const int J = std::max(1, gen_terms(ra));
     if (J > 16) return set_err(FT_EINVAL, "ft_solve_fast_modes: at most 14 forcing modes");
+    static const bool no_ode1 = getenv("FT_NO_ODE1") != nullptr;
+    if (!no_ode1 && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N)) {
+        // single-node (ODE) plans: B x N right-hand sides are a few KB, so generate the
+        // array (same device kernel as ft_assemble_rhs_modes) and run the one-kernel march
+        if (!p->oder_d && (rc = alloc_copy((void**)&p->oder_d, nullptr, sizeof(double) * rows_of(p) * p->N)))
+            return rc;
+        const bool u_dev = is_device_ptr(u);
+        double* X = u;
+        if (!u_dev) {
+            if ((rc = ensure_work(p))) return rc;
+            X = p->work_d;
+        }
+        ra.R = p->oder_d;
+        FT_CUDA(cudaEventRecord(p->ev0, st));
+        FT_CUDA(launch_rhs_modes(ra, st));
+        FT_CUDA(launch_ode_whole(X, p->oder_d, p->col_d, p->pc_d, p->N, p->B, st));
+        FT_CUDA(cudaEventRecord(p->ev1, st));
+        if (!u_dev) FT_CUDA(cudaMemcpyAsync(u, X, sizeof(double) * rows_of(p) * p->N, cudaMemcpyDeviceToHost, st));
+        FT_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        FT_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+        if (rep) {
+            std::snprintf(rep->method, sizeof(rep->method), "%s", "fast");
+            rep->iterations = 0;
+            rep->residual = 0.0;
+            rep->device_ms = ms;
+            rep->kernel_launches = 2;
+            rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        }
+        return FT_OK;
+    }
     const size_t ab = sizeof(double) * rows_of(p) * J, tb = sizeof(double) * (size_t)B * p->N * J;
     if (ab != p->genA_bytes) {
         if (p->genA_d) cudaFree(p->genA_d);
@@ -1570,7 +1602,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d};
+                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);
