@@ -331,7 +331,9 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         fms = f0.elapsed_time(f1) / args.steps
         fused = {"value": total_unknowns / (fms / 1e3), "unit": "unknowns/s", "ms_per_step": fms,
-                 "path": "ft_solve_fast_modes (RHS generated in the leaves; includes the per-call table setup)"}
+                 "path": ("ft_solve_fast_modes (single node: RHS array generated on the device, one-kernel march)"
+                          if plan.nodes == 1 else
+                          "ft_solve_fast_modes (RHS generated in the leaves; includes the per-call table setup)")}
 
     e2e = None
     if not args.no_e2e:
