@@ -1286,7 +1286,11 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     const cudaStream_t st = p->stream;
     const bool stream_rhs = fast && !rhs_dev && is_pinned_host(rhs);
     const bool stream_u = fast && !u_dev && is_pinned_host(u);
-    if ((stream_rhs || stream_u) && !getenv("FT_NO_STREAM")) return solve_streamed(p, rhs, u, rep, stream_rhs, t_start);
+    // single-node (ODE) plans move a few KB: one copy each way around the one-kernel march
+    const bool ode1 = fast && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N) &&
+                      !getenv("FT_NO_ODE1");
+    if ((stream_rhs || stream_u) && !ode1 && !getenv("FT_NO_STREAM"))
+        return solve_streamed(p, rhs, u, rep, stream_rhs, t_start);
     double* X;
     const double* src;
     if (u_dev) {

@@ -208,7 +208,8 @@ def test_in_place_and_device_buffers(ft, oracle_mod):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("cid,kw", [(4, dict(time_steps=4500, cells=4097)), (2, dict(time_steps=16384)),
-                                    (3, dict(time_steps=5000, cells=65)), (5, dict(time_steps=3000))])
+                                    (3, dict(time_steps=5000, cells=65)), (5, dict(time_steps=3000)),
+                                    (1, dict(time_steps=4096))])  # ODE: one copy each way, one kernel
 def test_streamed_host_solve(ft, oracle_mod, cid, kw):
     """Pinned host buffers take the streamed path (chunked H2D of R added by the
     leaves, D2H of finished chunks overlapping the solve); it must agree with the
