@@ -129,7 +129,17 @@ typedef struct ft_plan_info {
     uint64_t node_begin;   /* first interior node (0-based) held by this plan */
     uint64_t local_nodes;  /* nodes held by this plan (rows of its buffers per problem) */
     uint64_t slabs_local;  /* slabs (CTAs) of this rank */
+    uint64_t flags;        /* FT_PLAN_* bits: which fast-path kernels the plan's device-buffer solve runs */
 } ft_plan_info;
+
+enum {
+    FT_PLAN_SLAB_LEAF = 1,      /* multi-slab (space-time SPIKE) leaf */
+    FT_PLAN_FUSED_LEAF = 2,     /* one cooperative kernel per leaf */
+    FT_PLAN_FUSE0 = 4,          /* the n = 64 history products folded into the leaf */
+    FT_PLAN_CLUSTER_MP = 8,     /* K-CTA cluster history products (n = 8192, 16384) */
+    FT_PLAN_SPLIT_MP = 16,      /* split K-branch history products with a combine pass (n >= 32768) */
+    FT_PLAN_ODE_WHOLE = 32      /* single-node plans: the one-kernel march */
+};
 
 typedef struct ft_plan ft_plan;
 

@@ -94,6 +94,7 @@ def rlib():
         L.ref_toeplitz_gmres.argtypes = [P, P, U, D, U, P, C.POINTER(U)]
         L.ref_toeplitz_matvec.argtypes = [P, P, U, P, P]
         L.ref_block_matvec.argtypes = [P, P, U, U, D, P, P]
+        L.ref_setup.argtypes = [I, D, U, U, D, D, P, P, P, P, P, P]
         _r = L
     return _r
 
@@ -252,6 +253,26 @@ def ref_solve(s, method: str, F, u0=None, phi=None, tol=0.0, restart=0, max_iter
     if rc != 0:
         raise RuntimeError(L.ref_last_error().decode())
     return U, int(it.value), float(sec.value)
+
+
+def ref_setup(s, F=None, u0=None):
+    """The reference's own scheme assembly: (first column, second column (Scheme 2
+    B~) or None, off-block scale (Scheme 4) or None, assembled RHS (Scheme 4, when
+    F is given) or None)."""
+    L = rlib()
+    if L is None:
+        raise RuntimeError("reference library not built (oracle/build_ref.sh)")
+    N = s.time_steps
+    col = np.empty(N)
+    col2 = np.empty(N) if int(s.scheme) == OR_HYPER else None
+    off = C.c_double(0.0)
+    R = np.empty((s.space_cells - 1, N)) if (F is not None and int(s.scheme) == OR_DIFFUSION) else None
+    rc = L.ref_setup(int(s.scheme), s.gamma, N, s.space_cells, s.time_length, s.space_length, _d(F), _d(u0),
+                     col.ctypes.data, None if col2 is None else col2.ctypes.data, C.byref(off),
+                     None if R is None else R.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(L.ref_last_error().decode())
+    return col, col2, (off.value if int(s.scheme) == OR_DIFFUSION else None), R
 
 
 def toeplitz_case(n: int, seed: int, lower: bool = False):

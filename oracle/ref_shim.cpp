@@ -7,6 +7,8 @@
 //   fractime::lower_toeplitz_forward_solve        toeplitz.hpp:102 / toeplitz.cpp:169-186
 //   fractime::gmres_solve + make_toeplitz_operator krylov.cpp:107-223, toeplitz.cpp:204
 //   fractime::g_weights / m_weights / power_step   weights.cpp:8-40
+//   fractime::assemble_scheme2_reordered / assemble_scheme3_reordered / assemble_scheme4
+//                                                  schemes.cpp:149-167, :272-288, :381-410
 // Forcing / initial-data callbacks look values up in caller-supplied grids so
 // the reference and the GPU path see bit-identical inputs.
 #include <cmath>
@@ -132,6 +134,46 @@ int ref_ode_column(double gamma, uint64_t N, double time_length, double* col) {
         const auto g = g_weights(gamma, N);
         col[0] = 1.0 + k.mu * g.values[0];
         for (std::size_t j = 1; j < N; ++j) col[j] = k.mu * (g.values[j] - g.values[j - 1]);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Scheme setup through the reference's own assembly (schemes.cpp:149-167, :272-288,
+// :381-410): the Toeplitz first column (Scheme 2: A~ and B~) and, for Scheme 4,
+// the assembled right-hand side from grid callbacks (rhs may be null).
+int ref_setup(int scheme, double gamma, uint64_t time_steps, uint64_t space_cells, double time_length,
+              double space_length, const double* F, const double* u0, double* col, double* col2, double* off,
+              double* rhs) {
+    try {
+        ProblemSpec spec;
+        spec.scheme = scheme == 1 ? SchemeId::Hyperbolic : scheme == 2 ? SchemeId::DiffusionWave : SchemeId::Diffusion;
+        spec.gamma = gamma;
+        spec.time_steps = time_steps;
+        spec.space_cells = space_cells;
+        spec.time_length = time_length;
+        spec.space_length = space_length;
+        auto g = std::make_shared<Grids>(Grids{F, u0, nullptr, time_steps, space_cells, spec.h(), spec.tau(),
+                                               0.0, 0.0});
+        spec.forcing = [g](double x, double t) {
+            return g->F ? g->F[(node_of(*g, x) - 1) * g->N + (step_of(*g, t) - 1)] : 0.0;
+        };
+        if (u0) spec.initial_u0 = [g](double x) { return g->u0[node_of(*g, x) - 1]; };
+        const std::size_t N = time_steps;
+        if (scheme == 1) {
+            auto r = assemble_scheme2_reordered(spec);
+            std::memcpy(col, r.a_tilde.first_col().data(), sizeof(double) * N);
+            if (col2) std::memcpy(col2, r.b_tilde.first_col().data(), sizeof(double) * N);
+        } else if (scheme == 2) {
+            auto t = assemble_scheme3_reordered(spec);
+            std::memcpy(col, t.first_col().data(), sizeof(double) * N);
+        } else {
+            auto sys = assemble_scheme4(spec);
+            std::memcpy(col, sys.op.diag_block().first_col().data(), sizeof(double) * N);
+            if (off) *off = sys.op.off_block_scale();
+            if (rhs) std::memcpy(rhs, sys.rhs.data(), sizeof(double) * sys.rhs.size());
+        }
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

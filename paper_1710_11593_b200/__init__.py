@@ -83,7 +83,10 @@ class _Info(C.Structure):
                 ("leaf", C.c_uint64), ("levels", C.c_uint64), ("slabs", C.c_uint64),
                 ("h", C.c_double), ("tau", C.c_double), ("mu", C.c_double), ("c", C.c_double),
                 ("rank", C.c_int), ("world", C.c_int), ("node_begin", C.c_uint64), ("local_nodes", C.c_uint64),
-                ("slabs_local", C.c_uint64)]
+                ("slabs_local", C.c_uint64), ("flags", C.c_uint64)]
+
+
+PLAN_SLAB_LEAF, PLAN_FUSED_LEAF, PLAN_FUSE0, PLAN_CLUSTER_MP, PLAN_SPLIT_MP, PLAN_ODE_WHOLE = 1, 2, 4, 8, 16, 32
 
 
 FORCING_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_double, C.c_void_p)
@@ -147,15 +150,30 @@ def _check(rc: int) -> None:
         raise FractimeError(rc, msg)
 
 
-def _ptr(a) -> int:
-    """Device pointer of a torch tensor or host pointer of a numpy array."""
+def _ptr(a, count: Optional[int] = None, what: str = "buffer") -> int:
+    """Device pointer of a torch tensor or host pointer of a numpy array, after
+    checking dtype (float64), contiguity and, when given, the element count --
+    the C ABI takes plain pointers, so a wrong buffer would be written out of
+    bounds instead of failing."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.dtype == np.float64 and a.flags.c_contiguous
+        if a.dtype != np.float64:
+            raise InvalidArgument(-1, f"{what}: float64 expected, got {a.dtype}")
+        if not a.flags.c_contiguous:
+            raise InvalidArgument(-1, f"{what}: C-contiguous array expected")
+        if count is not None and a.size != count:
+            raise InvalidArgument(-1, f"{what}: {count} elements expected, got {a.size}")
         return a.ctypes.data
     if hasattr(a, "data_ptr"):
-        assert a.is_contiguous()
+        import torch
+
+        if a.dtype != torch.float64:
+            raise InvalidArgument(-1, f"{what}: torch.float64 expected, got {a.dtype}")
+        if not a.is_contiguous():
+            raise InvalidArgument(-1, f"{what}: contiguous tensor expected")
+        if count is not None and a.numel() != count:
+            raise InvalidArgument(-1, f"{what}: {count} elements expected, got {a.numel()}")
         return a.data_ptr()
     raise TypeError(f"unsupported buffer type {type(a)}")
 
@@ -239,6 +257,7 @@ class Plan:
                 rank, world = partition
                 _check(lib().ft_setup_partitioned(arr, C.byref(opt), rank, world, C.byref(h)))
         self._h = h
+        self._device = device
         info = _Info()
         _check(lib().ft_plan_get_info(self._h, C.byref(info)))
         self.info = info
@@ -291,25 +310,51 @@ class Plan:
         _check(lib().ft_assemble_rhs_grid(self._h, _ptr(F), _ptr(u0), _ptr(phi), out.ctypes.data))
         return out
 
+    def _mode_args(self, a, k, p, trig, u0amp, phiamp):
+        k = np.ascontiguousarray(k, dtype=np.float64).reshape(-1)
+        nm = k.size
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        trig = np.ascontiguousarray(trig, dtype=np.int32).reshape(-1)
+        for name, arr in (("a", a), ("p", p)):
+            if arr.size != self.B * nm:
+                raise InvalidArgument(-1, f"{name}: shape ({self.B}, {nm}) expected, got {arr.shape}")
+        if trig.size != nm:
+            raise InvalidArgument(-1, f"trig: {nm} entries expected, got {trig.size}")
+        u0amp = None if u0amp is None else np.ascontiguousarray(u0amp, dtype=np.float64).reshape(-1)
+        phiamp = None if phiamp is None else np.ascontiguousarray(phiamp, dtype=np.float64).reshape(-1)
+        for name, arr in (("u0amp", u0amp), ("phiamp", phiamp)):
+            if arr is not None and arr.size != self.B:
+                raise InvalidArgument(-1, f"{name}: {self.B} entries expected, got {arr.size}")
+        return a, k, p, trig, u0amp, phiamp
+
     def assemble_rhs_modes(self, out, a, k, p, trig, u0amp=None, phiamp=None):
         """Device generation of a separable forcing into the device buffer `out`."""
-        a = np.ascontiguousarray(a, dtype=np.float64)
-        k = np.ascontiguousarray(k, dtype=np.float64)
-        p = np.ascontiguousarray(p, dtype=np.float64)
-        trig = np.ascontiguousarray(trig, dtype=np.int32)
-        u0amp = None if u0amp is None else np.ascontiguousarray(u0amp, dtype=np.float64)
-        phiamp = None if phiamp is None else np.ascontiguousarray(phiamp, dtype=np.float64)
+        a, k, p, trig, u0amp, phiamp = self._mode_args(a, k, p, trig, u0amp, phiamp)
+        self._check_device(out, "rhs")
         _check(lib().ft_assemble_rhs_modes(self._h, len(k), a.ctypes.data, k.ctypes.data,
                                            p.ctypes.data, trig.ctypes.data,
                                            None if u0amp is None else u0amp.ctypes.data,
-                                           None if phiamp is None else phiamp.ctypes.data, _ptr(out)))
+                                           None if phiamp is None else phiamp.ctypes.data,
+                                           _ptr(out, self.shape[0] * self.shape[1], "rhs")))
         return out
+
+    def _check_device(self, buf, what):
+        if hasattr(buf, "is_cuda") and buf.is_cuda and int(self.info_device()) >= 0:
+            if buf.device.index != self.info_device():
+                raise InvalidArgument(-1, f"{what}: tensor on cuda:{buf.device.index}, plan on cuda:{self.info_device()}")
+
+    def info_device(self) -> int:
+        return getattr(self, "_device", -1)
 
     def _solve(self, fn, rhs, out):
         if out is None:
             out = np.empty(self.shape) if isinstance(rhs, np.ndarray) else rhs.new_empty(self.shape)
+        n = self.shape[0] * self.shape[1]
+        self._check_device(rhs, "rhs")
+        self._check_device(out, "u")
         rep = _Report()
-        _check(fn(self._h, _ptr(rhs), _ptr(out), C.byref(rep)))
+        _check(fn(self._h, _ptr(rhs, n, "rhs"), _ptr(out, n, "u"), C.byref(rep)))
         report = SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
                              rep.device_ms, rep.kernel_launches)
         return out, report
@@ -337,16 +382,13 @@ class Plan:
         """Fast solve with the separable forcing of assemble_rhs_modes generated
         inside the leaves (the right-hand side is never materialised); `out`
         (host or device, [rows][N]) receives U."""
-        a = np.ascontiguousarray(a, dtype=np.float64)
-        k = np.ascontiguousarray(k, dtype=np.float64)
-        p = np.ascontiguousarray(p, dtype=np.float64)
-        trig = np.ascontiguousarray(trig, dtype=np.int32)
-        u0amp = None if u0amp is None else np.ascontiguousarray(u0amp, dtype=np.float64)
-        phiamp = None if phiamp is None else np.ascontiguousarray(phiamp, dtype=np.float64)
+        a, k, p, trig, u0amp, phiamp = self._mode_args(a, k, p, trig, u0amp, phiamp)
+        self._check_device(out, "u")
         rep = _Report()
         _check(lib().ft_solve_fast_modes(self._h, len(k), a.ctypes.data, k.ctypes.data, p.ctypes.data,
                                          trig.ctypes.data, None if u0amp is None else u0amp.ctypes.data,
-                                         None if phiamp is None else phiamp.ctypes.data, _ptr(out), C.byref(rep)))
+                                         None if phiamp is None else phiamp.ctypes.data,
+                                         _ptr(out, self.shape[0] * self.shape[1], "u"), C.byref(rep)))
         return out, SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
                                 rep.device_ms, rep.kernel_launches)
 

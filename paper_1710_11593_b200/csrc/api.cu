@@ -114,11 +114,14 @@ struct ft_plan {
     double* respw_d = nullptr;    // multi-slab phase-2 injection responses (leaf_wbuild)
     std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
     std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf
+    double* leafcol_d = nullptr;         // device copy (LeafArgs::leafcol; per plan, so concurrent plans
+                                         // on distinct streams never share leaf weights)
     double kc_h[kKcLen] = {};            // problem 0's leaf constants (LeafArgs::kc)
     double* dw_d = nullptr;       // direct weights [B][N]
     double* cprime_d = nullptr;   // [B][nodes]
     double* den_d = nullptr;
     double* scratch_d = nullptr;  // [B][nodes]
+    unsigned* dmctr_d = nullptr;  // multi-CTA direct march step counters
     double* work_d = nullptr;     // staging for host buffers
     double* rdev_d = nullptr;     // streamed host solves: device copy of the caller's R
     cudaStream_t h2d_st = nullptr, d2h_st = nullptr;  // streamed host solves: copy engines
@@ -128,6 +131,7 @@ struct ft_plan {
     const void* graph_X = nullptr;
     const void* graph_src = nullptr;
     const void* graph_gen = nullptr;
+    int graph_genJ = 0;
     double* genA_d = nullptr;     // ft_solve_fast_modes tables
     double* genT_d = nullptr;
     size_t genA_bytes = 0, genT_bytes = 0;
@@ -143,6 +147,22 @@ struct ft_plan {
 namespace {
 
 uint64_t rows_of(const ft_plan* p) { return (uint64_t)p->B * (uint64_t)p->local_nodes; }
+
+// The n = 64 history products fold into the next cooperative slab leaf (wide
+// problems only: for config 3's two slabs the standalone product is cheaper,
+// 100 vs 102 ms); device-buffer solves without fused RHS generation.
+bool fuse0_plan(const ft_plan* p) {
+    static const bool off = getenv("FT_NO_FUSE0") != nullptr;
+    return !off && p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= 8 &&
+           !p->stencil;
+}
+
+// Single-node (ODE / Toeplitz) plans short enough for the one-kernel march
+// (ode_whole_kernel); FT_NO_ODE1 (read once) is the A/B switch back to the D&C.
+bool ode_whole_plan(const ft_plan* p) {
+    static const bool no_ode1 = getenv("FT_NO_ODE1") != nullptr;
+    return !no_ode1 && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N);
+}
 
 // ---- reference setup restated (weights.cpp / schemes.cpp) -------------------
 double power_step(uint64_t k, double p) {  // weights.cpp:8-16
@@ -563,6 +583,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     int rc;
     if ((rc = alloc_copy((void**)&p->pc_d, p->pc_h.data(), sizeof(ProblemConst) * B))) return rc;
     if ((rc = alloc_copy((void**)&p->col_d, p->col_h.data(), sizeof(double) * B * N))) return rc;
+    if ((rc = alloc_copy((void**)&p->leafcol_d, p->leafcol_h.data(), sizeof(double) * B * 32))) return rc;
     if ((rc = alloc_copy((void**)&p->wts_d, p->wts_h.data(), sizeof(double) * B * (N + 1)))) return rc;
     if ((rc = alloc_copy((void**)&p->lampow_d, lampow.data(), sizeof(double) * lampow.size()))) return rc;
     if ((rc = alloc_copy((void**)&p->dw_d, dw.data(), sizeof(double) * dw.size()))) return rc;
@@ -571,6 +592,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
         if ((rc = alloc_copy((void**)&p->den_d, den.data(), sizeof(double) * den.size()))) return rc;
     }
     if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * 2 * B * nodes))) return rc;
+    if ((rc = alloc_copy((void**)&p->dmctr_d, nullptr, 2 * sizeof(unsigned)))) return rc;
     if (p->stencil && (rc = alloc_copy((void**)&p->vsrc_d, nullptr, sizeof(double) * rows_of(p) * N))) return rc;
     if (p->multi) {
         if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
@@ -683,17 +705,11 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
              std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr, const GenRhs* gen = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
-    // in-leaf weights col[1..L) in constant memory (shared by all plans: set per solve;
-    // a captured graph gets them from its launcher)
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    FT_CUDA(cudaStreamIsCapturing(st, &cap));
-    if (cap == cudaStreamCaptureStatusNone) FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     uint64_t nl = 0;
     unsigned leaf_index = 0;
     // the n = 64 history products fold into the next (cooperative slab) leaf
     // (wide problems only: for config 3's two slabs the standalone product is cheaper, 100 vs 102 ms)
-    const bool fuse0 = p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= 8 &&
-                       !io && !gen && !p->stencil && getenv("FT_NO_FUSE0") == nullptr;
+    const bool fuse0 = fuse0_plan(p) && !io && !gen;
     bool pend0 = false, pend0_first = false;
     p->last_fuse0 = fuse0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
@@ -733,6 +749,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.P = p->P;
             a.pc = p->pc_d;
             a.col = p->col_d;
+            a.leafcol = p->leafcol_d;
             a.lampow = p->lampow_d;
             a.lp_stride = p->lp_stride;
             a.kcoef = p->kcoef_d;
@@ -1012,6 +1029,16 @@ int ft_plan_get_info(const ft_plan* p, ft_plan_info* info) {
     info->node_begin = p->node_begin;
     info->local_nodes = p->local_nodes;
     info->slabs_local = p->P_local;
+    uint64_t f = 0;
+    if (p->multi) f |= FT_PLAN_SLAB_LEAF;
+    if (p->multi && p->part_world == 1 && p->fused_leaf) f |= FT_PLAN_FUSED_LEAF;
+    if (fuse0_plan(p)) f |= FT_PLAN_FUSE0;
+    for (const auto& lv : p->levels) {
+        if (lv.K > 1 && !(lv.K >= p->split_min_k && p->split_k)) f |= FT_PLAN_CLUSTER_MP;
+        if (lv.K >= p->split_min_k && p->split_k) f |= FT_PLAN_SPLIT_MP;
+    }
+    if (ode_whole_plan(p)) f |= FT_PLAN_ODE_WHOLE;
+    info->flags = f;
     info->h = p->h;
     info->tau = p->tau;
     info->mu = p->mu[0];
@@ -1238,8 +1265,7 @@ static int solve_streamed(ft_plan* p, const double* rhs, double* u, ft_report* r
 static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* gen, uint64_t* launches) {
     const cudaStream_t st = p->stream;
     // single-node (ODE) problems: the whole time march in one kernel per call
-    static const bool no_ode1 = getenv("FT_NO_ODE1") != nullptr;  // A/B switch: the D&C schedule instead
-    if (!gen && !no_ode1 && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N)) {
+    if (!gen && ode_whole_plan(p)) {
         FT_CUDA(launch_ode_whole(X, src, p->col_d, p->pc_d, p->N, p->B, st));
         *launches = 1;
         return FT_OK;
@@ -1247,7 +1273,8 @@ static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* g
     const bool use_graph = (p->part_world == 1 || p->p2p) && !getenv("FT_NO_GRAPH");
     if (!use_graph) return run_fast(p, X, src, launches, nullptr, nullptr, gen);
     const void* gkey = gen ? (const void*)gen->A : nullptr;
-    if (!p->graph || p->graph_X != X || p->graph_src != src || p->graph_gen != gkey) {
+    const int gJ = gen ? gen->J : 0;
+    if (!p->graph || p->graph_X != X || p->graph_src != src || p->graph_gen != gkey || p->graph_genJ != gJ) {
         if (p->graph) cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
         cudaStream_t cs;
@@ -1268,8 +1295,8 @@ static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* g
         p->graph_X = X;
         p->graph_src = src;
         p->graph_gen = gkey;
+        p->graph_genJ = gJ;
     }
-    FT_CUDA(set_leaf_columns(p->leafcol_h.data(), p->B, st));
     FT_CUDA(cudaGraphLaunch(p->graph, st));
     *launches = p->graph_launches;
     return FT_OK;
@@ -1287,8 +1314,7 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
     const bool stream_rhs = fast && !rhs_dev && is_pinned_host(rhs);
     const bool stream_u = fast && !u_dev && is_pinned_host(u);
     // single-node (ODE) plans move a few KB: one copy each way around the one-kernel march
-    const bool ode1 = fast && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N) &&
-                      !getenv("FT_NO_ODE1");
+    const bool ode1 = fast && ode_whole_plan(p);
     if ((stream_rhs || stream_u) && !ode1 && !getenv("FT_NO_STREAM"))
         return solve_streamed(p, rhs, u, rep, stream_rhs, t_start);
     double* X;
@@ -1331,6 +1357,7 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
         da.scratch = p->scratch_d;
         da.scratch2 = p->scratch_d + (uint64_t)p->B * p->nodes;
         da.stencil = p->stencil ? 1 : 0;
+        da.ctr = p->dmctr_d;
         FT_CUDA(launch_direct(da, p->B, st));
         launches = 1;
     }
@@ -1426,8 +1453,7 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
     ra.cvals = c_d;
     const int J = std::max(1, gen_terms(ra));
     if (J > 16) return set_err(FT_EINVAL, "ft_solve_fast_modes: at most 14 forcing modes");
-    static const bool no_ode1 = getenv("FT_NO_ODE1") != nullptr;
-    if (!no_ode1 && p->kind == SK_DIAG && p->nodes == 1 && p->part_world == 1 && ode_whole_ok(p->N)) {
+    if (ode_whole_plan(p)) {
         // single-node (ODE) plans: B x N right-hand sides are a few KB, so generate the
         // array (same device kernel as ft_assemble_rhs_modes) and run the one-kernel march
         if (!p->oder_d && (rc = alloc_copy((void**)&p->oder_d, nullptr, sizeof(double) * rows_of(p) * p->N)))
@@ -1458,6 +1484,12 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
         return FT_OK;
     }
     const size_t ab = sizeof(double) * rows_of(p) * J, tb = sizeof(double) * (size_t)B * p->N * J;
+    if (ab != p->genA_bytes || tb != p->genT_bytes) {
+        // the captured graph bakes in the table pointers and J: a reallocation may hand
+        // back the same address, so drop the graph rather than trust the pointer key
+        if (p->graph) cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
     if (ab != p->genA_bytes) {
         if (p->genA_d) cudaFree(p->genA_d);
         p->genA_d = nullptr;
@@ -1605,8 +1637,8 @@ void ft_destroy(ft_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
-    void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
+    void* ptrs[] = {p->pc_d, p->col_d, p->leafcol_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
+                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->dmctr_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);

@@ -8,11 +8,101 @@
 //   Scheme 2 direct : src/schemes.cpp:210-232  (history :212-218, upwind march :219-228)
 //   ODE direct      : src/toeplitz.cpp:169-186 (lower_toeplitz_forward_solve)
 //   RHS             : src/schemes.cpp:401-408 (Scheme 4), :300-306 (Scheme3Rhs)
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace ftb {
 
 // One CTA per problem; the step loop runs inside the kernel.
+// The sequential spatial solve of step n for problem pb by one warp.  The chain
+// runs redundantly on every lane in the reference's order (same operations,
+// same rounding); each block of 32 nodes' operands is loaded coalesced one block
+// ahead and broadcast by shuffles, so the chain waits only on its own latency.
+__device__ __forceinline__ void dm_sweep(const DirectArgs& a, int pb, uint64_t n, int lane) {
+    const int nodes = a.nodes;
+    const uint64_t N = a.N;
+    double* rhs = a.scratch + (uint64_t)pb * nodes;
+    double* X = a.X + (uint64_t)pb * nodes * N;
+    const ProblemConst pc = a.pc[pb];
+    auto ld = [&](const double* p, int i) { return i < nodes ? __ldcg(p + i) : 0.0; };
+    if (a.kind == SK_DIAG) {
+        for (int i = lane; i < nodes; i += 32) X[(uint64_t)i * N + n] = __ldcg(rhs + i) / pc.d;
+        return;
+    }
+    if (a.kind == SK_TRIDIAG) {
+        const double* cp = a.cprime + (uint64_t)pb * nodes;
+        const double* dn = a.den + (uint64_t)pb * nodes;
+        const double off = -pc.off;
+        double prev = 0.0;
+        double r_cur = ld(rhs, lane), d_cur = ld(dn, lane);
+        for (int i0 = 0; i0 < nodes; i0 += 32) {  // forward: rhs[i] = (rhs[i] - off rhs[i-1]) / den[i]
+            const double r_nx = ld(rhs, i0 + 32 + lane), d_nx = ld(dn, i0 + 32 + lane);
+            double mine = 0.0;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const double v = __shfl_sync(0xffffffffu, r_cur, k), d = __shfl_sync(0xffffffffu, d_cur, k);
+                if (i0 + k < nodes) {
+                    prev = i0 + k == 0 ? v / d : (v - off * prev) / d;
+                    if (lane == k) mine = prev;
+                }
+            }
+            if (i0 + lane < nodes) rhs[i0 + lane] = mine;
+            r_cur = r_nx;
+            d_cur = d_nx;
+        }
+        __syncwarp();
+        // backward: rhs[i] -= cprime[i] rhs[i+1], i = nodes-2 .. 0 (rhs[nodes-1] is final)
+        double next = prev;
+        if (lane == 0) X[(uint64_t)(nodes - 1) * N + n] = next;
+        const int top = nodes - 1;  // blocks of 32 below node top, descending
+        auto ldb = [&](const double* p, int i) { return i >= 0 ? __ldcg(p + i) : 0.0; };
+        double rb = ldb(rhs, top - 1 - lane), cb = ldb(cp, top - 1 - lane);
+        for (int i0 = top - 1; i0 >= 0; i0 -= 32) {  // nodes i0, i0-1, ..., i0-31
+            const double rn = ldb(rhs, i0 - 32 - lane), cn = ldb(cp, i0 - 32 - lane);
+            double mine = 0.0;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const double v = __shfl_sync(0xffffffffu, rb, k), c = __shfl_sync(0xffffffffu, cb, k);
+                if (i0 - k >= 0) {
+                    next = v - c * next;
+                    if (lane == k) mine = next;
+                }
+            }
+            if (i0 - lane >= 0) X[(uint64_t)(i0 - lane) * N + n] = mine;
+            rb = rn;
+            cb = cn;
+        }
+        return;
+    }
+    // upwind marches (Scheme 3; Scheme 2 with the stencil history)
+    const double* hs = a.scratch2 + (uint64_t)pb * nodes;
+    double u_left = 0.0, hist_left = 0.0;
+    double r_cur = ld(rhs, lane), h_cur = a.stencil ? ld(hs, lane) : 0.0;
+    for (int i0 = 0; i0 < nodes; i0 += 32) {
+        const double r_nx = ld(rhs, i0 + 32 + lane), h_nx = a.stencil ? ld(hs, i0 + 32 + lane) : 0.0;
+        double mine = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const double v = __shfl_sync(0xffffffffu, r_cur, k), hk = __shfl_sync(0xffffffffu, h_cur, k);
+            if (i0 + k < nodes) {
+                double value;
+                if (a.stencil) {  // schemes.cpp:219-228 (pc.off = 1/h - c g0)
+                    value = (v + hist_left + pc.off * u_left) / pc.d;
+                    hist_left = hk;
+                } else {          // schemes.cpp:345-351
+                    value = (v + u_left / pc.h) / pc.d;
+                }
+                u_left = value;
+                if (lane == k) mine = value;
+            }
+        }
+        if (i0 + lane < nodes) X[(uint64_t)(i0 + lane) * N + n] = mine;
+        r_cur = r_nx;
+        h_cur = h_nx;
+    }
+}
+
 __global__ void __launch_bounds__(1024) direct_kernel(DirectArgs a) {
     const int pb = blockIdx.x;
     const uint64_t N = a.N;
@@ -85,10 +175,211 @@ __global__ void __launch_bounds__(1024) direct_kernel(DirectArgs a) {
     }
 }
 
+// ---- multi-CTA reference-order march (the on-device oracle at scale) ----------
+// Same arithmetic, same summation order as direct_kernel (bitwise equal), but the
+// per-node history sums run on every SM: each CTA owns groups of 32 rows (one
+// summing thread per row), the other warps stage the rows' solved prefixes
+// X[row][k0, k0 + kDmChunk) through double-buffered shared memory with coalesced
+// L2 loads (ld.global.cg: X is rewritten during the kernel, L1 could be stale).
+// The sequential spatial sweep (Thomas / upwind / divide, schemes.cpp:453-461,
+// :345-351) runs on extra warps of CTA 0 (dm_sweep, one warp per problem).  Steps are ordered by two monotonic
+// global counters: `hist` (CTAs that published step n's right-hand sides) and
+// `solved` (steps whose U the sweep has written).  For sums whose last term is
+// U(n-1) (every kind but the wave scheme, which adds w[1] U(n-1) first) the CTAs
+// form step n's partial sum over k < n-1 while the sweep is still solving step
+// n-1, then add the last term: the same order, so still bitwise.
+constexpr int kDmLoadWarps = 15;
+constexpr int kDmThreads = 32 * (1 + kDmLoadWarps);  // history warps (+ kDmSweepWarps sweep warps, CTA 0 only)
+constexpr int kDmSweepWarps = 4;                     // concurrent per-problem spatial sweeps (batched plans)
+constexpr int kDmChunk = 256;                        // time steps per staged tile (64 KB in flight per CTA)
+constexpr int kDmPitch = kDmChunk + 1;               // odd pitch: conflict-free column reads
+constexpr int kDmMaxGroups = 64;                     // row groups of 32 per CTA
+
+__device__ __forceinline__ unsigned dm_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void dm_st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dm_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * (1 + kDmLoadWarps)) : "memory"); }
+
+__global__ void __launch_bounds__(kDmThreads + 32 * kDmSweepWarps) direct_multi_kernel(DirectArgs a, unsigned* ctr, int rows,
+                                                                       int groups) {
+    extern __shared__ double dm_smem[];  // [2][32][kDmPitch] staged tiles, [kDmMaxGroups][32] partials, [2][kDmChunk] weights
+    double* part = dm_smem + 2 * 32 * kDmPitch;
+    unsigned* hist_cnt = ctr;
+    unsigned* solved = ctr + 1;
+    const uint64_t N = a.N;
+    const int nodes = a.nodes;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool pipelined = !(a.kind == SK_UPWIND && !a.stencil);
+    if (warp > kDmLoadWarps) {  // ---- the sequential spatial sweeps (CTA 0; one warp per problem) ----
+        if (blockIdx.x != 0) return;
+        const int B = rows / nodes;
+        const int sw = warp - 1 - kDmLoadWarps;
+        for (uint64_t n = 0; n < N; ++n) {
+            if (sw == 0 && lane == 0)
+                while (dm_ld_acquire(hist_cnt) < (unsigned)(n + 1) * gridDim.x) __nanosleep(32);
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * kDmSweepWarps) : "memory");
+            __threadfence();
+            for (int pb = sw; pb < B; pb += kDmSweepWarps)
+                dm_sweep(a, pb, n, lane);
+            __threadfence();
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * kDmSweepWarps) : "memory");
+            if (sw == 0 && lane == 0) dm_st_release(solved, (unsigned)(n + 1));
+        }
+        return;
+    }
+    // ---- history CTAs: groups g = blockIdx.x + j gridDim.x of 32 rows of one problem ----
+    const int gpp = (nodes + 31) / 32;  // row groups per problem
+    const int my_groups = groups > (int)blockIdx.x ? (groups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    double* wbuf = part + kDmMaxGroups * 32;  // [2][kDmChunk] weights w[n - k] of the staged chunk
+    auto group_row = [&](int j, int r, int& pb) {  // global row of lane r of the CTA's j-th group (-1: none)
+        const int g = (int)blockIdx.x + j * (int)gridDim.x;
+        pb = g / gpp;
+        const int i = (g % gpp) * 32 + r;
+        return i < nodes ? pb * nodes + i : -1;
+    };
+    auto wait_solved = [&](unsigned target) {
+        if (tid == 0)
+            while (dm_ld_acquire(solved) < target) __nanosleep(64);
+        dm_bar();
+    };
+    for (uint64_t n = 0; n < N; ++n) {
+        // terms of the pre-sum: k in [0, kp); pipelined kinds leave k = n-1 for later
+        const uint64_t kp = n >= 1 ? n - 1 : 0;
+        wait_solved(pipelined ? (unsigned)kp : (unsigned)n);
+        const int nch = (int)((kp + kDmChunk - 1) / kDmChunk);
+        const int items = my_groups * nch;
+        // item it = (group j, chunk c); loaders fill buf[it & 1] one item ahead of the summers
+        auto load_item = [&](int it) {
+            const int j = it / nch, c = it % nch;
+            const uint64_t k0 = (uint64_t)c * kDmChunk;
+            const int len = (int)(kp - k0 < (uint64_t)kDmChunk ? kp - k0 : (uint64_t)kDmChunk);
+            double* buf = dm_smem + (it & 1) * 32 * kDmPitch;
+            int pb = 0;
+            for (int e = tid - 32; e < 32 * kDmChunk; e += 32 * kDmLoadWarps) {
+                const int r = e / kDmChunk, q = e % kDmChunk;
+                const int row = group_row(j, r, pb);
+                if (row >= 0 && q < len) buf[r * kDmPitch + q] = __ldcg(a.X + (uint64_t)row * N + k0 + q);
+            }
+            group_row(j, 0, pb);
+            const double* w = a.w + (uint64_t)pb * N;
+            for (int q = tid - 32; q < len; q += 32 * kDmLoadWarps) wbuf[(it & 1) * kDmChunk + q] = __ldg(w + (n - k0 - q));
+        };
+        double acc = 0.0;  // summer lane's running sum (current group)
+        if (warp >= 1 && items > 0) load_item(0);
+        dm_bar();
+        for (int it = 0; it < items; ++it) {
+            if (warp >= 1) {
+                if (it + 1 < items) load_item(it + 1);
+            } else {
+                const int j = it / nch, c = it % nch;
+                int pb = 0;
+                const int row = group_row(j, lane, pb);
+                const uint64_t k0 = (uint64_t)c * kDmChunk;
+                const int len = (int)(kp - k0 < (uint64_t)kDmChunk ? kp - k0 : (uint64_t)kDmChunk);
+                const double* buf = dm_smem + (it & 1) * 32 * kDmPitch + lane * kDmPitch;
+                const double* wv = wbuf + (it & 1) * kDmChunk;  // wv[q] = w[n - k0 - q]
+                if (c == 0) acc = 0.0;
+                if (row >= 0) {
+                    const double* w = a.w + (uint64_t)pb * N;
+                    if (a.kind == SK_DIAG && c == 0) acc = __ldcg(a.X + (uint64_t)row * N + n);
+                    if (a.kind == SK_UPWIND && !a.stencil && c == 0) acc += w[1] * __ldcg(a.X + (uint64_t)row * N + n - 1);
+                    // one dependent add per term in the reference's order; the smem operands of the
+                    // next terms are independent and issued ahead (unrolled)
+                    int q = 0;
+                    if (a.kind == SK_DIAG) {
+                        for (; q + 8 <= len; q += 8) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) acc -= wv[q + u] * buf[q + u];
+                        }
+                        for (; q < len; ++q) acc -= wv[q] * buf[q];
+                    } else {
+                        for (; q + 8 <= len; q += 8) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) acc += wv[q + u] * buf[q + u];
+                        }
+                        for (; q < len; ++q) acc += wv[q] * buf[q];
+                    }
+                }
+                if (c == nch - 1) part[j * 32 + lane] = acc;
+            }
+            dm_bar();
+        }
+        // finish step n: (pipelined) the last term k = n-1 once the sweep has solved it
+        if (pipelined) wait_solved((unsigned)n);
+        if (warp == 0) {
+            for (int j = 0; j < my_groups; ++j) {
+                int pb = 0;
+                const int row = group_row(j, lane, pb);
+                if (row < 0) continue;
+                const int i = row - pb * nodes;
+                const double* xi = a.X + (uint64_t)row * N;
+                const double* w = a.w + (uint64_t)pb * N;
+                const ProblemConst& pc = a.pc[pb];
+                double s = nch > 0 ? part[j * 32 + lane] : 0.0;
+                double r;
+                if (a.kind == SK_DIAG) {
+                    if (nch == 0) s = __ldcg(xi + n);
+                    if (n >= 1) s -= w[1] * __ldcg(xi + n - 1);
+                    r = s;
+                } else if (a.kind == SK_UPWIND && !a.stencil) {
+                    if (nch == 0 && n >= 1) s += w[1] * __ldcg(xi + n - 1);
+                    r = __ldcg(xi + n) - s;
+                } else {
+                    if (n >= 1) s += w[1] * __ldcg(xi + n - 1);
+                    if (a.kind == SK_TRIDIAG) {
+                        r = __ldcg(xi + n) + pc.c * s;
+                    } else {  // Scheme 2 stencil
+                        r = __ldcg(xi + n) + s;
+                        a.scratch2[(uint64_t)pb * nodes + i] = s;
+                    }
+                }
+                a.scratch[row] = r;
+            }
+        }
+        dm_bar();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(hist_cnt, 1u);
+        }
+    }
+}
+
+size_t direct_multi_smem() { return sizeof(double) * (2 * 32 * kDmPitch + kDmMaxGroups * 32 + 2 * kDmChunk); }
+
 cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st) {
-    int threads = a.nodes < 1024 ? ((a.nodes + 31) / 32) * 32 : 1024;
-    direct_kernel<<<B, threads, 0, st>>>(a);
-    return cudaGetLastError();
+    const int rows = B * a.nodes;
+    static const bool single = getenv("FT_DIRECT_SINGLE") != nullptr;  // A/B: the one-CTA-per-problem march
+    if (single || a.ctr == nullptr) {
+        int threads = a.nodes < 1024 ? ((a.nodes + 31) / 32) * 32 : 1024;
+        direct_kernel<<<B, threads, 0, st>>>(a);
+        return cudaGetLastError();
+    }
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = direct_multi_smem();
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(direct_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, direct_multi_kernel, kDmThreads + 32 * kDmSweepWarps, smem);
+    if (e != cudaSuccess) return e;
+    const int groups = B * ((a.nodes + 31) / 32);  // groups never straddle problems (one weight row each)
+    int ctas = std::min(groups, sms * std::max(occ, 1));
+    ctas = std::max(ctas, (groups + kDmMaxGroups - 1) / kDmMaxGroups);
+    if (ctas > sms * occ) return cudaErrorInvalidConfiguration;  // more rows than the partial buffers hold
+    e = cudaMemsetAsync(a.ctr, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    DirectArgs aa = a;
+    unsigned* ctr = a.ctr;
+    int r = rows, g = groups;
+    void* args[] = {&aa, &ctr, &r, &g};
+    return cudaLaunchCooperativeKernel((const void*)direct_multi_kernel, dim3(ctas), dim3(kDmThreads + 32 * kDmSweepWarps), args,
+                                       smem, st);
 }
 
 // ---- device RHS generation (separable forcing) -------------------------------
@@ -337,13 +628,13 @@ cudaError_t launch_ode_whole(double* X, const double* R, const double* col, cons
                              int B, cudaStream_t st) {
     const bool sc = 2 * N * sizeof(double) <= kOdeSmem;
     const size_t smem = (sc ? 2 : 1) * N * sizeof(double);
-    static bool set = false;
-    if (!set) {
+    static DeviceOnce set;
+    if (set.first()) {
         cudaError_t e = cudaFuncSetAttribute(ode_whole_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOdeSmem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ode_whole_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOdeSmem);
         if (e != cudaSuccess) return e;
-        set = true;
+        set.done();
     }
     if (sc)
         ode_whole_kernel<true><<<B, kOdeThreads, smem, st>>>(X, R, col, pc, N);

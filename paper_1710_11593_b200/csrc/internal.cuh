@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -35,7 +36,7 @@ constexpr int kLeafThreads = 256;
 constexpr int kKcPow = 32, kKcLamW = 37, kKcLam = 38, kKcV1 = 40, kKcNv = 48, kKcCol2 = 56, kKcLen = 88;
 // (kKcCol2: col[32..64), the far half of the level-0 history window fused into the leaf)
 constexpr int kMaxSlabs = 160;
-constexpr int kMaxLeafProblems = 128;  // problems per plan (in-leaf weights in constant memory)  // slabs per problem in the multi-slab leaf
+constexpr int kMaxLeafProblems = 128;  // problems per plan
 constexpr int kMpThreads = 256;
 constexpr int kMpTile = 4096;   // complex points per CTA (64 KiB of SMEM + pad)
 constexpr int kMpDirectMaxH = 64;   // blocks n <= 128 use the direct Toeplitz kernel
@@ -59,6 +60,20 @@ __device__ __forceinline__ cplx ldgc(const cplx* p) {
 }
 __host__ __device__ inline cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
 __host__ __device__ inline cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
+
+// Per-device one-time setup (cudaFuncSetAttribute applies to the current device
+// only; plans may pick a device through ft_options.device).  Two threads racing
+// both run the (idempotent) setup.
+struct DeviceOnce {
+    std::atomic<unsigned long long> mask{0};
+    static int dev() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return d & 63;
+    }
+    bool first() const { return !((mask.load() >> dev()) & 1ull); }
+    void done() { mask.fetch_or(1ull << dev()); }
+};
 
 // ---- programmatic dependent launch (PDL) ------------------------------------
 // Every kernel of the fast-solve schedule is launched with programmatic stream
@@ -122,6 +137,7 @@ struct LeafArgs {
     int P;                     // slabs (CTAs) per problem
     const ProblemConst* pc;    // [B]
     const double* col;         // [B][N] Toeplitz first columns
+    const double* leafcol;     // [B][32] in-leaf weights col[1..32) (entry 0 and entries >= N are 0), plan-owned
     const double* lampow;      // [B][lp_stride]: lam^k, k = 0..lp_stride-1
     int lp_stride;
     const double* kcoef;       // [B][2][nodes] single-CTA Dirichlet coefficients kF, kB
@@ -185,6 +201,7 @@ struct DirectArgs {
     double* scratch;      // [B][nodes]
     double* scratch2;     // [B][nodes] (Scheme 2: per-node history of the current step)
     int stencil;          // Scheme 2 (kind SK_UPWIND)
+    unsigned* ctr;        // multi-CTA march: [2] step counters (null: one CTA per problem)
 };
 
 struct RhsModesArgs {
@@ -229,7 +246,6 @@ cudaError_t launch_direct(const DirectArgs& a, int B, cudaStream_t st);
 bool ode_whole_ok(uint64_t N);
 cudaError_t launch_ode_whole(double* X, const double* R, const double* col, const ProblemConst* pc, uint64_t N,
                              int B, cudaStream_t st);
-cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
 int gen_terms(const RhsModesArgs& a);  // J of the separable RHS tables
 cudaError_t launch_gen_tables(const RhsModesArgs& a, double* A, double* T, cudaStream_t st);

@@ -34,9 +34,6 @@ namespace ftb {
 
 constexpr int kLeafUnroll = FT_LEAF_UNROLL;
 
-// in-leaf history weights col[1..L) per problem, read through the constant
-// cache (CTA-uniform: the compiler keeps them in uniform registers)
-__constant__ double c_leafcol[kMaxLeafProblems][32];
 
 template <int NPT>
 struct ScanConsts {
@@ -84,20 +81,24 @@ struct LeafConsts<false, NPT, L> {
 #if FT_LEAF_WREG
     double w[L];
 #else
-    const double* w;  // this problem's row of c_leafcol: read per use through the constant cache
-                      // (CTA-uniform index; 31 weights in registers spilled)
+    const double* w;  // this problem's row of the plan's leaf weights (LeafArgs::leafcol), read per
+                      // use through the read-only path (CTA-uniform; 31 weights in registers spilled)
 #endif
     __device__ __forceinline__ LeafConsts(const LeafArgs& a, int pb, const double* lp, double lam, int lane) {
         scan_consts<NPT>(sc, lp, a.lp_stride, lam, lane);
-        const double* cc = c_leafcol[pb < kMaxLeafProblems ? pb : 0];
+        const double* cc = a.leafcol + 32 * (size_t)pb;
 #if FT_LEAF_WREG
 #pragma unroll
-        for (int j = 0; j < L; ++j) w[j] = cc[j];
+        for (int j = 0; j < L; ++j) w[j] = __ldg(cc + j);
 #else
         w = cc;
 #endif
     }
+#if FT_LEAF_WREG
     __device__ __forceinline__ double cw(int j) const { return w[j]; }
+#else
+    __device__ __forceinline__ double cw(int j) const { return __ldg(w + j); }
+#endif
     __device__ __forceinline__ double lam() const { return sc.lam; }
     __device__ __forceinline__ double stepF(int d, double y, double S, int) const { return fma(sc.pwF[d], y, S); }
     __device__ __forceinline__ double stepB(int d, double y, double S, int) const { return fma(sc.pwB[d], y, S); }
@@ -939,14 +940,14 @@ cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st) {
 template <int KIND, int NPT, int L>
 static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool multi, cudaStream_t st) {
     const size_t osmem = sizeof(double) * (size_t)kLeafThreads * NPT * (L + 1);
-    static bool oattr = false;
-    if (!oattr) {
+    static DeviceOnce oattr;
+    if (oattr.first()) {
         const int mx = (int)(sizeof(double) * kLeafThreads * NPT * (L + 1));
         cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(leaf_kernel<KIND, NPT, L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        oattr = true;
+        oattr.done();
     }
     const dim3 blk(KIND == SK_DIAG ? threads : kLeafThreads);
     if (!multi) {
@@ -960,11 +961,11 @@ static cudaError_t launch_leaf_t(const LeafArgs& a, int ctas, int threads, bool 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)a.slab * (L + 1));
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(leaf_correct<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
-        attr = true;
+        attr.done();
     }
     return launch_ex(leaf_correct<KIND, NPT, L>, dim3(ctas), dim3(kLeafThreads), smem, st, 1, a);
 }
@@ -972,13 +973,13 @@ static cudaError_t launch_correct_t(const LeafArgs& a, int ctas, cudaStream_t st
 template <int KIND, int NPT, int L>
 static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
         cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
-        attr = true;
+        attr.done();
     }
     // cooperative attribute through cudaLaunchKernelEx: capturable into the solve's CUDA graph
     cudaLaunchConfig_t cfg = {};
@@ -998,12 +999,12 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
 template <int KIND, int NPT, int L>
 static cudaError_t launch_p2p_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (attr.first()) {
         const int mx = (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1)));
         cudaFuncSetAttribute(leaf_fused_p2p<KIND, NPT, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(leaf_fused_p2p<KIND, NPT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        attr = true;
+        attr.done();
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
@@ -1051,11 +1052,6 @@ cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double
     else if (kind == SK_UPWIND) leaf_wbuild<SK_UPWIND, 32><<<grid, threads, 0, st>>>(a, W);
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
-}
-
-cudaError_t set_leaf_columns(const double* cols_host, int problems, cudaStream_t st) {
-    return cudaMemcpyToSymbolAsync(c_leafcol, cols_host, sizeof(double) * 32 * problems, 0,
-                                   cudaMemcpyHostToDevice, st);
 }
 
 // Supported (kind, NPT, L): register tile of NPT*L doubles per thread.

@@ -935,13 +935,13 @@ static uint64_t split_batch_bytes() {
 
 template <int K, int LOGM>
 static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(mp_kernel<K, LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
         cudaFuncSetAttribute(mp_kernel<K, LOGM, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
-        attr_set = true;
+        attr_set.done();
     }
     // pre-fold measured faster for K = 16 (n = 65536: 63.5 -> 52.0 ms per level), slower
     // for K = 8 (42.8 -> 46.4 ms: the extra scratch round trip outweighs the K-fold re-reads)
@@ -977,12 +977,12 @@ static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
 template <int K, int LOGM>
 static cudaError_t launch_mp_k(const MpArgs& a, int groups, cudaStream_t st) {
     if (a.scratch) return launch_mp_split<K, LOGM>(a, st);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(mp_kernel<K, LOGM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, (1 << LOGM) > kMpTile ? (1 << LOGM) : kMpTile));
         if (K > 8) cudaFuncSetAttribute(mp_kernel<K, LOGM, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr_set = true;
+        attr_set.done();
     }
     return launch_ex(mp_kernel<K, LOGM, false>, dim3(K, groups, 1), dim3(kMpThreads), mp_smem_bytes(a.G, a.m), st,
                      (unsigned)K, a);
@@ -992,10 +992,10 @@ template <int H>
 static cudaError_t launch_direct_h(const MpArgs& a, cudaStream_t st) {
     constexpr int RPC = kDirThreads / (H / (H < 16 ? H : 16));
     const size_t smem = sizeof(double) * 2 * RPC * (H + 1);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(mp_direct_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
+        attr_set.done();
     }
     const int ctas = (a.rows + RPC - 1) / RPC;
     return launch_ex(mp_direct_kernel<H>, dim3(ctas), dim3(kDirThreads), smem, st, 1, a);
@@ -1015,20 +1015,20 @@ static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
 #define FT_MP1_SMEM_PAD 0
 #endif
     const size_t smem = mp_smem_bytes(G, n) + FT_MP1_SMEM_PAD;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(mp1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
+        attr_set.done();
     }
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
     const int ctas = (npairs + G - 1) / G;
     if constexpr (n <= kMpTile) {
         static const bool cta_sync = getenv("FT_MP1_CTA") != nullptr;  // A/B switch
         if (!cta_sync) {
-            static bool gattr = false;
-            if (!gattr) {
+            static DeviceOnce gattr;
+            if (gattr.first()) {
                 cudaFuncSetAttribute(mp1g_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                gattr = true;
+                gattr.done();
             }
             return launch_ex(mp1g_kernel<LOGN>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
         }
@@ -1040,11 +1040,11 @@ template <int LOGN>
 static cudaError_t launch_spec1(const double* col, uint64_t N, int B, int J, cplx* spec, const cplx* tw,
                                 cudaStream_t st) {
     constexpr int n = 1 << LOGN;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(spec1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, n));
-        attr_set = true;
+        attr_set.done();
     }
     spec1_kernel<LOGN><<<B, kMpThreads, mp_smem_bytes(1, n), st>>>(col, N, J, spec, tw);
     return cudaGetLastError();
@@ -1105,11 +1105,11 @@ cudaError_t launch_mp(const MpArgs& a, int groups, cudaStream_t st) {
 
 cudaError_t launch_spectra(const double* col, uint64_t N, int B, int n, int m, int K, int J,
                            cplx* spec, const cplx* tw, int logT, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)mp_smem_bytes(1, kMpBranchMax));
-        attr_set = true;
+        attr_set.done();
     }
     SpecArgs a{col, N, n, m, K, J, spec, tw, logT};
     spectra_kernel<<<dim3(K, B), kMpThreads, mp_smem_bytes(1, m), st>>>(a);

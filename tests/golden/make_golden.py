@@ -94,6 +94,13 @@ def main():
         else:
             U, _, _ = oracle.ref_solve(s, "direct", F, u0, phi)
             data[f"{name}_direct"] = U
+            # the reference's own setup: first column(s) and (Scheme 4) the assembled RHS
+            col, col2, _, R = oracle.ref_setup(s, F, u0)
+            data[f"{name}_col"] = col
+            if col2 is not None:
+                data[f"{name}_col2"] = col2
+            if R is not None:
+                data[f"{name}_rhs"] = R
     np.savez_compressed(Path(__file__).with_name("golden.npz"), **data)
     Path(__file__).with_name("tables.json").write_text(json.dumps(parse_tables(), indent=1))
     print("wrote", len(data), "arrays")
