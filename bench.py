@@ -10,8 +10,12 @@ A step is one ft_solve_fast over the device-resident right-hand side
 is needed).  `e2e` runs the same solve through the C ABI with pinned HOST
 buffers (H2D of the RHS and D2H of the solution inside the timed region).
 `--impl reference` times the unmodified reference CPU solver (oracle/_ref,
-built from /root/reference by oracle/build_ref.sh) on a bounded sample of the
-same workload using all host cores.
+built from /root/reference by oracle/build_ref.sh) on the same workload: its
+direct march (the only reference path that runs at these sizes) on M' nodes at
+the full N, scaled linearly to the full M (see reference_estimate); both arms
+print BASELINE.json's metric string.  Without --no-configs the line also carries
+per-config sub-results for BASELINE configs 1, 2, 3 and 5 (ours and the
+reference's, measured the same way).
 """
 from __future__ import annotations
 
@@ -29,6 +33,18 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def _metric() -> str:
+    """BASELINE.json's metric string, printed identically by both arms."""
+    p = ROOT / "BASELINE.json"
+    try:
+        return json.loads(p.read_text())["metric"]
+    except Exception:  # noqa: BLE001
+        return "space-time unknowns solved/sec (M\u00b7N/s, fp64) and % of HBM roofline at 1/2/4/8 B200"
+
+
+METRIC = _metric()
 
 
 def peaks():
@@ -139,83 +155,210 @@ def max_over_ranks(world, value: float) -> float:
 
 
 # ---- CPU reference arm / cpu_baseline -----------------------------------------
+#
+# The reference solves one problem on one thread (SPEC.md: single-threaded per
+# solve; its thread pool only runs independent ladder rows), and its fast path
+# (GMRES) is infeasible or fails on configs 2-5.  Its direct march
+# costs O(M N^2): every node sums its whole history at every step, the same work
+# per node.  A sample of M' nodes at the FULL N therefore measures the per-node
+# cost in the regime of the real solve (long history rows), and the full-size
+# time is that sample times M / M' (linear in M: exact in work; the sample's rows
+# are cache-resident, so if anything this flatters the reference).  The raw rate
+# of a full-M time prefix (N' = 128, short rows) is reported beside it.
 
-def reference_sample(cid: int, n_prefix: int, threads: int):
-    """One bounded sample: `threads` concurrent runs of the unmodified reference
-    direct solver (the only reference path that runs at this size; its GMRES fast
-    path is infeasible) on the time prefix N' of the workload at
-    full M (tau = 1/N bit-exactly).  Returns (unknowns/s, seconds, info)."""
+REF_SAMPLE_NODES = {4: 2, 2: 4, 3: 2, 5: 4}   # M' of the per-config reduced-M full-N sample
+
+
+def _ref_one(w, method="direct"):
+    """One reference solve through its public API (oracle/_ref: the unmodified
+    reference + a C-ABI shim) or, where it is not built, the C port; returns seconds."""
+    import oracle
+
+    F = oracle.forcing_grid(w)
+    u0 = oracle.initial_grid(w, w.u0amp)
+    phi = oracle.initial_grid(w, w.phiamp)
+    if oracle.rlib() is not None:
+        t0 = time.perf_counter()
+        if int(w.specs[0].scheme) == 0:  # config 1: the Toeplitz-level API (SURVEY.md 3.4)
+            raise ValueError("use _ref_cfg1")
+        oracle.ref_solve(w.specs[0], method, F, u0, phi)
+        return time.perf_counter() - t0, "reference"
+    t0 = time.perf_counter()
+    oracle.direct(w, F, u0, phi)
+    return time.perf_counter() - t0, "port"
+
+
+def _ref_cfg1():
+    """Config 1 at full size through the reference Toeplitz API: direct
+    (lower_toeplitz_forward_solve, toeplitz.cpp:169-186) and fast (gmres_solve on
+    make_toeplitz_operator(embed_circulant(T)), krylov.cpp:107-223, tol 1e-10)."""
+    import ctypes as C
+
     import numpy as np
 
     import oracle
     from paper_1710_11593_b200 import workloads as W
 
-    L = oracle.rlib()
-    kind = "reference"
-    if L is None:
-        kind = "port"
-    w = W.config(cid, time_steps=n_prefix)
-    F = oracle.forcing_grid(w)
-    u0 = oracle.initial_grid(w, w.u0amp)
+    w = W.config(1)
     s = w.specs[0]
-    res = [None] * threads
-
-    def run(i):
+    N = s.time_steps
+    L = oracle.rlib()
+    col = np.empty(N)
+    R = oracle.rhs(w, oracle.forcing_grid(w), oracle.initial_grid(w, w.u0amp))[0].copy()
+    x = np.empty(N)
+    if L is None:
+        oracle.olib().or_col_ode(s.gamma, N, s.tau(), col.ctypes.data)
         t0 = time.perf_counter()
-        if kind == "reference":
-            oracle.ref_solve(s, "direct", F, u0)
-        else:
-            oracle.direct(w, F, u0)
-        res[i] = time.perf_counter() - t0
-
+        oracle.olib().or_forward_solve(col.ctypes.data, R.ctypes.data, N, x.ctypes.data)
+        return {"direct_s": time.perf_counter() - t0, "fast_s": None, "kind": "port"}
+    L.ref_ode_column(s.gamma, N, s.time_length, col.ctypes.data)
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=run, args=(i,)) for i in range(threads)]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
-    wall = time.perf_counter() - t0
-    unknowns = threads * w.nodes * n_prefix
-    return unknowns / wall, wall, {"kind": kind, "nodes": w.nodes, "n_prefix": n_prefix}
+    L.ref_forward_solve(col.ctypes.data, R.ctypes.data, N, x.ctypes.data)
+    td = time.perf_counter() - t0
+    it = C.c_uint64(0)
+    t0 = time.perf_counter()
+    rc = L.ref_toeplitz_gmres(col.ctypes.data, R.ctypes.data, N, 1e-10, 40, x.ctypes.data, C.byref(it))
+    tf = time.perf_counter() - t0
+    return {"direct_s": td, "fast_s": tf, "fast_matvecs": int(it.value), "fast_converged": rc == 0,
+            "kind": "reference"}
+
+
+def reference_estimate(cid: int):
+    """Full-size reference direct-solve time for config `cid` from a reduced-M,
+    full-N sample (see the block comment above).  Returns a dict with value
+    (unknowns/s of the full workload), the sample and its law."""
+    from paper_1710_11593_b200 import workloads as W
+
+    full = W.config(cid)
+    if cid == 1:
+        r = _ref_cfg1()
+        best = r["direct_s"]
+        return {"value": full.unknowns / best, "full_solve_s": best, "kind": r["kind"], "cores": 1,
+                "sample": "full size (N = 4096): reference lower_toeplitz_forward_solve (direct) and "
+                          "gmres_solve on its FFT operator (fast); value from the faster (direct)",
+                "direct_s": r["direct_s"], "fast_s": r["fast_s"], "fast_matvecs": r.get("fast_matvecs"),
+                "law": "measured at full size (no extrapolation)"}
+    mp = REF_SAMPLE_NODES[cid]
+    w = W.config(cid, cells=mp + 1, batch=1 if cid == 5 else None)
+    t, kind = _ref_one(w)
+    per_problem = t * full.nodes / mp
+    problems = full.B
+    cores = os.cpu_count() or 1
+    # independent problems (config 5) run concurrently on all host cores, as the
+    # reference's harness pool would; one problem uses one core
+    lanes = min(cores, problems)
+    full_s = per_problem * math.ceil(problems / lanes)
+    return {"value": full.unknowns / full_s, "full_solve_s": full_s, "kind": kind, "cores": lanes,
+            "sample": f"reference solve(spec, Direct) on M'={mp} nodes at the full N={full.N} "
+                      f"(gamma {w.specs[0].gamma:.4g}, h = 1/{full.specs[0].space_cells}): {t:.3f} s",
+            "law": f"T_full = T(M') * M / M' (direct march: identical O(N^2) work per node)"
+                   + (f"; {problems} independent problems over {lanes} cores" if problems > 1 else ""),
+            "fast": ("infeasible at this size (GMRES: thousands of O(M N log N) matvecs, SURVEY.md P3)"
+                     if cid != 3 else "fails (GMRES does not converge at M = 1024, SURVEY.md P4)")}
+
+
+def reference_prefix_rate(cid: int, n_prefix: int = 128):
+    """Raw rate of the full-M time prefix N' (short history rows; side field)."""
+    from paper_1710_11593_b200 import workloads as W
+
+    w = W.config(cid, time_steps=n_prefix, batch=1 if cid == 5 else None)
+    t, kind = _ref_one(w)
+    return {"value": w.unknowns / t, "seconds": t, "sample": f"full M={w.nodes}, time prefix N'={n_prefix}"}
 
 
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    n_prefix = args.ref_prefix
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, wall, info = reference_sample(args.config, n_prefix, cores)
-        if i >= args.warmup:
-            vals.append((v, wall))
-    value = sum(v for v, _ in vals) / len(vals)
-    ms = 1e3 * sum(w for _, w in vals) / len(vals)
     from paper_1710_11593_b200 import workloads as W
 
     wl = W.config(args.config)
-    N = wl.N
-    # O(M N^2) direct-march law from the sample to the full size (labelled extrapolation)
-    full_s = (ms / 1e3) * (N / n_prefix) ** 2  # each core ran one whole sample solve
+    vals = []
+    est = None
+    for i in range(args.warmup + args.steps):
+        est = reference_estimate(args.config)
+        if i >= args.warmup:
+            vals.append(est["value"])
+    value = sum(vals) / len(vals)
+    ms = 1e3 * wl.unknowns / value
+    subs = {}
+    if not args.no_configs and args.config == 4:
+        for cid in (1, 2, 3, 5):
+            subs[f"cfg{cid}"] = reference_estimate(cid)
     line = {
         "impl": "reference",
-        "metric": "space-time unknowns solved/sec (M*N/s, fp64)",
+        "metric": METRIC,
         "value": value, "unit": "unknowns/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.name, "nodes": wl.nodes, "time_steps": N, "problems": wl.B,
-                   "sample_time_steps": n_prefix, "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": cores, "kind": info["kind"],
-                         "sample": f"{cores} concurrent reference direct solves of the time prefix "
-                                   f"N'={n_prefix} at full M={wl.nodes} (tau = 1/{N} exactly); "
-                                   f"the reference fast path (GMRES) is infeasible at this size",
-                         "extrapolated_full_solve_s_one_core": full_s},
+        "config": {"workload": wl.name, "nodes": wl.nodes, "time_steps": wl.N, "problems": wl.B,
+                   "parallelism": f"{est['cores']} host thread(s): the reference solves one problem per thread"},
+        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": est["cores"], "kind": est["kind"],
+                         "sample": est["sample"], "law": est["law"], "full_solve_s": est["full_solve_s"]},
         "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "prefix_rate": reference_prefix_rate(args.config) if args.config != 1 else None,
+        "configs": subs,
     }
     print(json.dumps(line), flush=True)
 
 
 # ---- our arm -------------------------------------------------------------------
+
+def _events_ms(stream, fn, steps):
+    import torch
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def measure_config(cid: int, steps: int, warmup: int, e2e_steps: int):
+    """Our numbers for one BASELINE config on one GPU (sub-results of the main
+    line): device-resident solve (CUDA events), and e2e through the C ABI with the
+    forcing modes in and U out to pinned host memory."""
+    import torch
+
+    import paper_1710_11593_b200 as ft
+    from paper_1710_11593_b200 import workloads as W
+
+    wl = W.config(cid)
+    plan = ft.Plan(wl.specs)
+    stream = torch.cuda.Stream()
+    plan.set_stream(stream.cuda_stream)
+    rhs = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    u = torch.empty_like(rhs)
+    plan.assemble_rhs_modes(rhs, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
+    torch.cuda.synchronize()
+    for _ in range(warmup):
+        _, rep = plan.solve_fast(rhs, u)
+    ms = _events_ms(stream, lambda: plan.solve_fast(rhs, u), steps)
+    h_u = torch.empty(plan.shape, dtype=torch.float64, pin_memory=True)
+    un = h_u.numpy()
+    plan.solve_fast_modes(un, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.solve_fast_modes(un, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    bpu = bytes_per_unknown(wl.N)
+    pk, _ = peaks()
+    out = {"workload": wl.name, "nodes": wl.nodes, "time_steps": wl.N, "problems": wl.B,
+           "value": wl.unknowns / (ms / 1e3), "unit": "unknowns/s", "ms_per_step": ms,
+           "hbm_roofline_frac": bpu * wl.unknowns / (ms / 1e3) / 1e9 / float(pk["hbm_gbs"]),
+           "kernel_launches_per_solve": int(rep.kernel_launches),
+           "e2e": {"value": wl.unknowns / e2e_s, "unit": "unknowns/s", "ms_per_step": 1e3 * e2e_s,
+                   "h2d_bytes_per_step": int(8 * (wl.a.size + wl.k.size + wl.p.size + wl.trig.size + 3 * wl.B)),
+                   "d2h_bytes_per_step": int(8 * wl.unknowns),
+                   "path": "ft_solve_fast_modes: forcing modes in, U out to pinned host memory"}}
+    del rhs, u, h_u, plan
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
 
 def run_ours(args, world, rank, local):
     import numpy as np
@@ -225,6 +368,12 @@ def run_ours(args, world, rank, local):
     from paper_1710_11593_b200 import workloads as W
 
     torch.cuda.set_device(local)
+    # the other BASELINE configs first (one GPU, rank 0 of a single-rank run), so
+    # config 4's 69 GB of buffers are not resident at the same time
+    subs = {}
+    if world == 1 and args.config == 4 and not args.no_configs:
+        for cid in (1, 2, 3, 5):
+            subs[f"cfg{cid}"] = {"ours": measure_config(cid, args.steps, max(3, args.warmup), args.e2e_steps)}
     wl = W.config(args.config, time_steps=args.time_steps or None)
     sharded = world > 1 and wl.B == 1 and wl.nodes > 2048
     if sharded:
@@ -288,32 +437,36 @@ def run_ours(args, world, rank, local):
     bpu = bytes_per_unknown(wl.N)
     solve_gbs = bpu * total_unknowns / (ms / 1e3) / 1e9 / world  # per GPU
 
-    # dominant kernel: per-launch device times of one profiled solve
-    ops = plan.profile_fast(rhs, u)
-    mp = [o for o in ops if o["kind"] == 1 and o["bytes"] > 0]  # (n = 64 products folded into leaves: 0 bytes)
-    lf = [o for o in ops if o["kind"] == 0]
-    mp_ms = sum(o["ms"] for o in mp)
-    lf_ms = sum(o["ms"] for o in lf)
-    mp_bytes = sum(o["bytes"] for o in mp)
-    lf_bytes = sum(o["bytes"] for o in lf)
-    dom = "mp_kernel" if mp_ms >= lf_ms else "leaf_kernel"
-    d_ms, d_bytes, d_n = (mp_ms, mp_bytes, len(mp)) if dom == "mp_kernel" else (lf_ms, lf_bytes, len(lf))
+    # dominant kernel: per-launch device times of one profiled solve of the path that is timed
+    traffic, traffic_note, per_level = None, None, {}
+    if int(plan.info.flags) & ft.PLAN_ODE_WHOLE:
+        # single-node plans run ONE kernel per solve (ode_whole_kernel): its launch is the solve
+        dom, d_ms, d_bytes, d_n = "ode_whole_kernel", ms, bpu * unknowns, 1
+        mp_ms, lf_ms, mp_bytes, lf_bytes = 0.0, ms, 0, bpu * unknowns
+    else:
+        ops = plan.profile_fast(rhs, u)
+        mp = [o for o in ops if o["kind"] == 1 and o["bytes"] > 0]  # (n = 64 products folded into leaves: 0 bytes)
+        lf = [o for o in ops if o["kind"] == 0]
+        mp_ms = sum(o["ms"] for o in mp)
+        lf_ms = sum(o["ms"] for o in lf)
+        mp_bytes = sum(o["bytes"] for o in mp)
+        lf_bytes = sum(o["bytes"] for o in lf)
+        dom = "mp_kernel" if mp_ms >= lf_ms else "leaf_kernel"
+        d_ms, d_bytes, d_n = (mp_ms, mp_bytes, len(mp)) if dom == "mp_kernel" else (lf_ms, lf_bytes, len(lf))
+        # DRAM traffic per launch of the dominant kernel: each level's algorithmic
+        # bytes scaled by the ncu-measured DRAM/algorithmic ratio of its kernel family
+        if dom == "mp_kernel" and d_n:
+            leaf_len = int(plan.info.leaf)
+            dram = sum(o["bytes"] * NCU_DRAM_OVER_ALG[mp_family(2 * leaf_len << o["level"])] for o in mp)
+            traffic = dram / d_n
+            traffic_note = ("bytes per launch (DRAM read+write), per-level ncu ratios " + json.dumps(NCU_DRAM_OVER_ALG)
+                            + f"; algorithmic bytes per launch {d_bytes / d_n:.4g}")
+        for o in mp:
+            lv = per_level.setdefault(o["level"], {"launches": 0, "ms": 0.0, "bytes": 0})
+            lv["launches"] += 1
+            lv["ms"] += o["ms"]
+            lv["bytes"] += o["bytes"]
     achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
-    # DRAM traffic per launch of the dominant kernel: each level's algorithmic
-    # bytes scaled by the ncu-measured DRAM/algorithmic ratio of its kernel family
-    traffic, traffic_note = None, None
-    if dom == "mp_kernel" and d_n:
-        leaf_len = int(plan.info.leaf)
-        dram = sum(o["bytes"] * NCU_DRAM_OVER_ALG[mp_family(2 * leaf_len << o["level"])] for o in mp)
-        traffic = dram / d_n
-        traffic_note = ("bytes per launch (DRAM read+write), per-level ncu ratios " + json.dumps(NCU_DRAM_OVER_ALG)
-                        + f"; algorithmic bytes per launch {d_bytes / d_n:.4g}")
-    per_level = {}
-    for o in mp:
-        lv = per_level.setdefault(o["level"], {"launches": 0, "ms": 0.0, "bytes": 0})
-        lv["launches"] += 1
-        lv["ms"] += o["ms"]
-        lv["bytes"] += o["bytes"]
 
     # the same solve with the separable forcing generated inside the leaves
     # (ft_solve_fast_modes: no RHS array, no RHS read -- SURVEY.md 8f item 2)
@@ -321,15 +474,8 @@ def run_ours(args, world, rank, local):
     if not sharded and plan.B == wl.B and not args.no_fused:
         plan.solve_fast_modes(u, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
         torch.cuda.synchronize()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            f0.record(stream)
-            for _ in range(args.steps):
-                plan.solve_fast_modes(u, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
-            f1.record(stream)
-        torch.cuda.synchronize()
-        fms = f0.elapsed_time(f1) / args.steps
+        fms = _events_ms(stream, lambda: plan.solve_fast_modes(u, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp),
+                         args.steps)
         fused = {"value": total_unknowns / (fms / 1e3), "unit": "unknowns/s", "ms_per_step": fms,
                  "path": ("ft_solve_fast_modes (single node: RHS array generated on the device, one-kernel march)"
                           if plan.nodes == 1 else
@@ -374,17 +520,17 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cores = os.cpu_count() or 1
-        v, wall, info = reference_sample(args.config, args.ref_prefix, cores)
-        cpu = {"value": v, "unit": "unknowns/s", "cores": cores, "kind": info["kind"],
-               "sample": f"{cores} concurrent reference direct solves (oracle/_ref) of the time prefix "
-                         f"N'={args.ref_prefix} at full M={wl.nodes}; wall {wall:.2f} s",
-               "extrapolated_full_solve_s_one_core": wall * (wl.N / args.ref_prefix) ** 2,
-               "extrapolation": "O(M N^2) direct-march law from the N' sample (one solve per core)"}
+        est = reference_estimate(args.config)
+        cpu = {"value": est["value"], "unit": "unknowns/s", "cores": est["cores"], "kind": est["kind"],
+               "sample": est["sample"], "law": est["law"], "full_solve_s": est["full_solve_s"],
+               "prefix_rate": reference_prefix_rate(args.config) if args.config != 1 else None}
+        if subs:
+            for cid in (1, 2, 3, 5):
+                subs[f"cfg{cid}"]["reference"] = reference_estimate(cid)
 
     if rank == 0:
         line = {
-            "metric": "space-time unknowns solved/sec (M*N/s, fp64) and % of HBM roofline",
+            "metric": METRIC,
             "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -405,6 +551,7 @@ def run_ours(args, world, rank, local):
             "e2e": e2e,
             "fused_rhs": fused,
             "cpu_baseline": cpu,
+            "configs": subs,
             "gpu_launches": launches_per_solve * args.steps,
             "clocks": clk.summary(),
         }
@@ -419,7 +566,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--time-steps", type=int, default=0, help="time-prefix variant (default: full N)")
-    ap.add_argument("--ref-prefix", type=int, default=128)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config sub-results (cfg1/2/3/5)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

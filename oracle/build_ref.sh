@@ -1,9 +1,10 @@
 #!/usr/bin/env bash
 # Build the UNMODIFIED reference library from its sources where they lie under
 # /root/reference (read-only; nothing is copied into this repo) plus our C-ABI
-# shim into oracle/_ref/libfractime_ref.so.  Flags mirror the reference's CMake
-# Release build (proj/CMakeLists.txt: C++20, -O3 default; we use -O2 and the
-# x86-64 baseline ISA, i.e. no FMA contraction, as the survey's probes did).
+# shim into oracle/_ref/libfractime_ref.so.  Flags are the reference's own CMake
+# Release build (proj/CMakeLists.txt: C++20, CMAKE_BUILD_TYPE Release -> -O3
+# -DNDEBUG, no -march: the x86-64 baseline ISA, so no FMA contraction -- the
+# results stay bitwise equal to the oracle's restatement, tests/test_oracle.py).
 # The output directory oracle/_ref/ is git-ignored but travels to the GPU box.
 set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"
@@ -19,7 +20,7 @@ objs=()
 for s in "${srcs[@]}"; do
   o="$out/$s.o"
   if [ ! -f "$o" ] || [ "$ref/src/$s.cpp" -nt "$o" ]; then
-    g++ -std=c++20 -O2 -fPIC -I"$ref/include" -c "$ref/src/$s.cpp" -o "$o"
+    g++ -std=c++20 -O3 -DNDEBUG -fPIC -I"$ref/include" -c "$ref/src/$s.cpp" -o "$o"
   fi
   objs+=("$o")
 done
