@@ -51,7 +51,11 @@
  *     every compute entry point fails with FT_ECUDA.
  *   - Threading: a plan is immutable after setup apart from its staging
  *     buffers; use one plan per host thread (distinct plans may run
- *     concurrently on distinct streams).
+ *     concurrently on distinct streams: every plan owns its device tables).
+ *   - Limits: N <= 65536 time steps (FT_ELENGTH otherwise: the history-product
+ *     kernels go up to n = 65536 points); at most 160 slabs of 512 nodes
+ *     (81920 interior nodes) per problem and 128 problems per plan (FT_EINVAL);
+ *     device memory ~ 2 x rows x N x 8 bytes for device-buffer solves.
  */
 #ifndef FRACTIME_B200_H
 #define FRACTIME_B200_H
@@ -110,7 +114,9 @@ typedef struct ft_options {
 typedef struct ft_report {
     char method[16];       /* "fast" / "direct" (SolveReport::method) */
     uint64_t iterations;   /* 0: both paths are direct methods (no Krylov matvecs) */
-    double residual;       /* 0 (as for the reference's direct path) */
+    double residual;       /* always 0: both paths are direct solves (no iteration, no residual
+                              estimate), as the reference's Direct path reports 0 (SolveReport
+                              defaults, schemes.hpp:58-63); parity is checked against the oracle */
     double seconds;        /* wall time of the call (SolveReport::seconds) */
     double device_ms;      /* device time of the solve proper (CUDA events) */
     uint64_t kernel_launches;  /* kernels this library launched for the call */

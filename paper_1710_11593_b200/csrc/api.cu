@@ -393,6 +393,9 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             (a.scheme != FT_SCHEME_ODE && a.space_cells != z.space_cells))
             return set_err(FT_EINVAL, "ft_setup_batch: problems must share scheme, N and M");
     }
+    if (probs[0].time_steps > kMaxTimeSteps)  // history-product kernels exist up to n = 65536 (K <= 16 branches)
+        return set_err(FT_ELENGTH, "ft_setup: at most " + std::to_string(kMaxTimeSteps) +
+                                       " time steps per problem are supported");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();

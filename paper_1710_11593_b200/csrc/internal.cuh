@@ -30,6 +30,7 @@ struct ProblemConst {
 };
 
 constexpr int kLeafThreads = 256;
+constexpr uint64_t kMaxTimeSteps = 65536;  // N limit (FT_ELENGTH): history products up to n = 65536
 // LeafArgs::kc layout (single-problem plans): in-leaf weights col[0..32), then
 // the uniform scan multipliers lam^(NPT 2^d) (d < 5), lam^(32 NPT), lam,
 // lam^(v+1) and lam^(NPT-v) (v < 8).

@@ -54,6 +54,27 @@ def test_validation_messages():
         ft.Plan(ft.ProblemSpec(ft.SchemeId.Diffusion, 0.5, 8, 1))
 
 
+def test_length_limit():
+    """N beyond the history-product kernels fails at setup with FT_ELENGTH (the
+    reference's std::length_error class), before any device use."""
+    with pytest.raises(ft.FractimeError, match="at most 65536 time steps") as e:
+        ft.Plan(ft.ProblemSpec(ft.SchemeId.Diffusion, 0.5, 65537, 4))
+    assert e.value.code == -3
+
+
+def test_buffer_checks_without_device():
+    """The Python binding rejects wrong host buffers before the C ABI sees them."""
+    from paper_1710_11593_b200 import _ptr
+
+    with pytest.raises(ft.InvalidArgument, match="float64"):
+        _ptr(np.zeros(4, dtype=np.float32))
+    with pytest.raises(ft.InvalidArgument, match="contiguous"):
+        _ptr(np.zeros((4, 4))[:, ::2])
+    with pytest.raises(ft.InvalidArgument, match="elements"):
+        _ptr(np.zeros(5), 4)
+    assert _ptr(np.zeros(4), 4) != 0
+
+
 @pytest.mark.parametrize("N,L", [(1, 32), (31, 32), (32, 32), (33, 32), (200, 32), (1000, 16), (4096, 32),
                                  (65536, 32), (777, 8)])
 def test_schedule_covers_history_exactly_once(N, L):
