@@ -113,9 +113,8 @@ struct ft_plan {
     double* resph_d = nullptr;
     double* respw_d = nullptr;    // multi-slab phase-2 injection responses (leaf_wbuild)
     std::vector<long double> lamL, G0L;  // long-double scan parameters (tables)
-    std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf
-    double* leafcol_d = nullptr;         // device copy (LeafArgs::leafcol; per plan, so concurrent plans
-                                         // on distinct streams never share leaf weights)
+    std::vector<double> leafcol_h;       // [B][32] col[0..32) (0 beyond N) for the leaf (batched plans:
+                                         // uploaded to the constant bank by leaf_bank_acquire)
     double kc_h[kKcLen] = {};            // problem 0's leaf constants (LeafArgs::kc)
     double* dw_d = nullptr;       // direct weights [B][N]
     double* cprime_d = nullptr;   // [B][nodes]
@@ -586,7 +585,6 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     int rc;
     if ((rc = alloc_copy((void**)&p->pc_d, p->pc_h.data(), sizeof(ProblemConst) * B))) return rc;
     if ((rc = alloc_copy((void**)&p->col_d, p->col_h.data(), sizeof(double) * B * N))) return rc;
-    if ((rc = alloc_copy((void**)&p->leafcol_d, p->leafcol_h.data(), sizeof(double) * B * 32))) return rc;
     if ((rc = alloc_copy((void**)&p->wts_d, p->wts_h.data(), sizeof(double) * B * (N + 1)))) return rc;
     if ((rc = alloc_copy((void**)&p->lampow_d, lampow.data(), sizeof(double) * lampow.size()))) return rc;
     if ((rc = alloc_copy((void**)&p->dw_d, dw.data(), sizeof(double) * dw.size()))) return rc;
@@ -685,6 +683,22 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     return FT_OK;
 }
 
+// Holds the batched-plan leaf weight bank for the enqueue of one solve.
+struct BankScope {
+    const ft_plan* p;
+    bool on;
+    cudaError_t err = cudaSuccess;
+    BankScope(const ft_plan* plan, bool enable) : p(plan), on(enable) {
+        if (on) {
+            err = leaf_bank_acquire(p, p->leafcol_h.data(), p->B, p->stream);
+            if (err != cudaSuccess) on = false;  // acquire unlocked on failure
+        }
+    }
+    ~BankScope() {
+        if (on) leaf_bank_release(p, p->stream);
+    }
+};
+
 // Streamed host solve: the caller's R arrives in time chunks of C steps on a
 // copy stream and is added by the leaf that solves those steps (history
 // products accumulate into a zeroed X, linear in R); finished chunks of U
@@ -708,6 +722,12 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
              std::vector<cudaEvent_t>* evs = nullptr, StreamIO* io = nullptr, const GenRhs* gen = nullptr) {
     const cudaStream_t st = p->stream;
     const uint64_t N = p->N;
+    // batched plans read their leaf weights from the per-device constant bank: own it for
+    // the enqueue (a captured graph gets it from launch_fast at each replay)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    FT_CUDA(cudaStreamIsCapturing(st, &cap));
+    BankScope bank(p, p->B > 1 && cap == cudaStreamCaptureStatusNone);
+    if (bank.err != cudaSuccess) return set_err(FT_ECUDA, "leaf weight bank upload failed");
     uint64_t nl = 0;
     unsigned leaf_index = 0;
     // the n = 64 history products fold into the next (cooperative slab) leaf
@@ -752,7 +772,6 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.P = p->P;
             a.pc = p->pc_d;
             a.col = p->col_d;
-            a.leafcol = p->leafcol_d;
             a.lampow = p->lampow_d;
             a.lp_stride = p->lp_stride;
             a.kcoef = p->kcoef_d;
@@ -1300,7 +1319,11 @@ static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* g
         p->graph_gen = gkey;
         p->graph_genJ = gJ;
     }
-    FT_CUDA(cudaGraphLaunch(p->graph, st));
+    {
+        BankScope bank(p, p->B > 1);
+        if (bank.err != cudaSuccess) return set_err(FT_ECUDA, "leaf weight bank upload failed");
+        FT_CUDA(cudaGraphLaunch(p->graph, st));
+    }
     *launches = p->graph_launches;
     return FT_OK;
 }
@@ -1638,9 +1661,10 @@ int ft_profile_fast(ft_plan* p, const double* rhs, double* u, ft_op_time* out, u
 
 void ft_destroy(ft_plan* p) {
     if (!p) return;
+    leaf_bank_forget(p);
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
-    void* ptrs[] = {p->pc_d, p->col_d, p->leafcol_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
+    void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
                     p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->dmctr_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);

@@ -138,7 +138,6 @@ struct LeafArgs {
     int P;                     // slabs (CTAs) per problem
     const ProblemConst* pc;    // [B]
     const double* col;         // [B][N] Toeplitz first columns
-    const double* leafcol;     // [B][32] in-leaf weights col[1..32) (entry 0 and entries >= N are 0), plan-owned
     const double* lampow;      // [B][lp_stride]: lam^k, k = 0..lp_stride-1
     int lp_stride;
     const double* kcoef;       // [B][2][nodes] single-CTA Dirichlet coefficients kF, kB
@@ -248,6 +247,11 @@ bool ode_whole_ok(uint64_t N);
 cudaError_t launch_ode_whole(double* X, const double* R, const double* col, const ProblemConst* pc, uint64_t N,
                              int B, cudaStream_t st);
 cudaError_t launch_rhs_modes(const RhsModesArgs& a, cudaStream_t st);
+// batched plans' in-leaf weights live in one constant bank per device: acquire it (waits for
+// the previous owner's last solve, uploads) before enqueueing a solve, release right after
+cudaError_t leaf_bank_acquire(const void* plan, const double* cols_host, int problems, cudaStream_t st);
+cudaError_t leaf_bank_release(const void* plan, cudaStream_t st);
+void leaf_bank_forget(const void* plan);
 int gen_terms(const RhsModesArgs& a);  // J of the separable RHS tables
 cudaError_t launch_gen_tables(const RhsModesArgs& a, double* A, double* T, cudaStream_t st);
 cudaError_t launch_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y,

@@ -110,3 +110,42 @@ def test_buffer_validation(ft):
         plan.solve_fast(good.t())
     with pytest.raises(ft.InvalidArgument):
         plan.solve_fast_modes(good, w.a[:, :2], w.k, w.p, w.trig)
+
+
+def test_concurrent_batched_plans_on_distinct_streams(ft):
+    """Two batched plans (per-problem leaf weights in the device's constant bank)
+    solving concurrently from two host threads on two streams give exactly their
+    serial results (the bank is handed over in stream order, ft_destroy forgets it)."""
+    import threading
+
+    import torch
+
+    wa = W.config(5, time_steps=2048, batch=3)
+    wb = W.config(5, time_steps=2048, batch=5)
+    wb.specs = [ft.ProblemSpec(s.scheme, 0.95 - s.gamma, s.time_steps, s.space_cells, s.time_length,
+                               s.space_length) for s in wb.specs]
+    out = {}
+    for name, w in (("a", wa), ("b", wb)):
+        plan = ft.Plan(w.specs)
+        R = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+        plan.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+        U, _ = plan.solve_fast(R, torch.empty_like(R))
+        out[name] = (plan, R, U.clone())
+    errs = []
+
+    def worker(name):
+        plan, R, ref = out[name]
+        st = torch.cuda.Stream()
+        plan.set_stream(st.cuda_stream)
+        U = torch.empty_like(R)
+        for _ in range(6):
+            plan.solve_fast(R, U)
+            if not torch.equal(U, ref):
+                errs.append(name)
+
+    ths = [threading.Thread(target=worker, args=(n,)) for n in ("a", "b")]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
