@@ -46,13 +46,22 @@ def torch_exchange(send: torch.Tensor, recv: torch.Tensor, stream=None, group=No
     backend = dist.get_backend(group)
 
     def run(count: int) -> None:
-        assert send.numel() == count and recv.numel() == count * dist.get_world_size(group)
+        world = dist.get_world_size(group)
+        if send.numel() != count or recv.numel() != count * world:
+            raise ValueError(f"exchange: {count} doubles per rank, buffers {send.numel()} / {recv.numel()}")
         ctx = torch.cuda.stream(stream) if (stream is not None and send.is_cuda) else _null()
         with ctx:
             if backend == "nccl":
                 dist.all_gather_into_tensor(recv, send, group=group)
+            elif send.is_cuda:
+                # gloo moves host tensors: stage through the host (the copy waits for this
+                # rank's phase-1 kernel on `stream`; the result lands before the correction)
+                host = send.cpu()
+                parts = [torch.empty_like(host) for _ in range(world)]
+                dist.all_gather(parts, host, group=group)
+                recv.copy_(torch.cat(parts))
             else:
-                parts = list(recv.view(dist.get_world_size(group), -1).unbind(0))
+                parts = list(recv.view(world, -1).unbind(0))
                 dist.all_gather(parts, send, group=group)
 
     return run

@@ -137,3 +137,57 @@ def test_sharded_plan_matches_single(ft, oracle_mod, world, cells, steps, scheme
     assert np.array_equal(U, U1)
     if cells <= 4097:
         assert oracle_mod.relerr(U, oracle_mod.direct(w, F, u0)) <= 1e-10
+
+
+def _sharded_worker(rank, world, port, cells, steps, q):
+    """One rank of a slab-partitioned config-4-shaped solve in its own process (own CUDA
+    context on the shared GPU), the default ShardedPlan exchange (torch_exchange over
+    gloo: the per-leaf carry all-gather is host-synchronous, so no kernel waits on the
+    other process)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        w = W.config(4, time_steps=steps, cells=cells)
+        p = par.ShardedPlan(w.specs[0], rank, world)
+        R = torch.empty(p.shape, dtype=torch.float64, device="cuda")
+        p.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig)  # this rank's rows of the device RHS
+        U, rep = p.solve_fast(R, torch.empty_like(R))
+        q.put((rank, p.node_begin, U.cpu().numpy(), int(rep.kernel_launches)))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, -1, traceback.format_exc(), 0))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cells,steps", [(2, 4097, 300), (4, 8193, 160)])
+def test_sharded_plan_two_processes_gloo(ft, world, cells, steps):
+    """ShardedPlan across `world` processes through torch.distributed (gloo): the
+    stitched solution is bitwise equal to the single-plan solve."""
+    import paper_1710_11593_b200 as ftm
+
+    w = W.config(4, time_steps=steps, cells=cells)
+    single = ftm.Plan(w.specs)
+    R = torch.empty(single.shape, dtype=torch.float64, device="cuda")
+    single.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig)
+    U1, _ = single.solve_fast(R, torch.empty_like(R))
+    U1 = U1.cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, cells, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for rank, begin, U, _ in res:
+        assert begin >= 0, U
+    U = np.vstack([r[2] for r in res])
+    assert [r[1] for r in res] == sorted(r[1] for r in res)
+    assert np.array_equal(U, U1)
