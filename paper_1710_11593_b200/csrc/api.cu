@@ -594,12 +594,12 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     }
     if ((rc = alloc_copy((void**)&p->scratch_d, nullptr, sizeof(double) * 2 * B * nodes))) return rc;
     if ((rc = alloc_copy((void**)&p->dmctr_d, nullptr, 2 * sizeof(unsigned)))) return rc;
+    if ((rc = alloc_copy((void**)&p->dbgclk_d, nullptr, sizeof(long long) * 16))) return rc;
     if (p->stencil && (rc = alloc_copy((void**)&p->vsrc_d, nullptr, sizeof(double) * rows_of(p) * N))) return rc;
     if (p->multi) {
         if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
         p->xsend_d = p->xch_d;
         if ((rc = alloc_copy((void**)&p->bar_d, nullptr, sizeof(unsigned)))) return rc;
-        if ((rc = alloc_copy((void**)&p->dbgclk_d, nullptr, sizeof(long long) * 16))) return rc;
         {
             // the fused leaf needs every slab CTA co-resident (cooperative launch)
             int dev_sms = 0, per_sm = 0;

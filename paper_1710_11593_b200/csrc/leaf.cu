@@ -349,6 +349,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     // node) staged through shared memory, then into the register window
     stage_rows<L>(s_out, a.src, a.radd, rowb, N, a.t0, mreal, len);
     __syncthreads();
+    if (stamp) a.dbg_clk[15] = clock64();
     double tile[NPT][L];
 #pragma unroll
     for (int v = 0; v < NPT; ++v) {
@@ -365,6 +366,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
             __syncthreads();
             stage_rows<L>(s_out, a.X, nullptr, rowb, N, a.t0 - L, mreal, L);
             __syncthreads();
+            if (stamp) a.dbg_clk[5] = clock64();
 #pragma unroll
             for (int v = 0; v < NPT; ++v) {
                 const int q = tid * NPT + v;
@@ -452,11 +454,13 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         double xleft = 0.0;  // upwind: solution at the node left of this thread's first node
         if (KIND == SK_DIAG) {
 #pragma unroll
-            for (int v = 0; v < NPT; ++v) x[v] = tile[v][0] / pc.d;
+            for (int v = 0; v < NPT; ++v) x[v] = tile[v][0] * pc.G0;  // G0 = 1/d (a DDIV is ~430 cycles)
         } else {
             double in[NPT];
 #pragma unroll
-            for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] / pc.d : tile[v][0];
+            // upwind: r / d as r * (1/d) -- a division on the step's critical path costs ~430 cycles
+            // on B200 (measured), the product 8; same rounding model as the host tables (local_solve_ld)
+            for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] * pc.G0 : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
             cta_scan<KIND, NPT, MODE == 0>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB, xleft);
             double cF = totF;
@@ -877,9 +881,12 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
     double* s_c0 = s_dyn;
     double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
+    const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) a.dbg_clk[12] = clock64();
     prefetch_correct_tables<L>(a);
     leaf_body<KIND, NPT, L, 1, PC>(a, s_x, false);
     __syncthreads();
+    if (stamp) a.dbg_clk[14] = clock64();
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(a.bar, 1u);
@@ -889,6 +896,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
         } while (v < a.bar_target);
     }
     __syncthreads();
+    if (stamp) a.dbg_clk[13] = clock64();
     correct_body<KIND, NPT, L>(a, s_c0, s_x, true);
 }
 
