@@ -22,6 +22,8 @@ import numpy as np
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libfractime_b200.so"
+if __import__("os").environ.get("FT_LIB_VARIANT"):  # A/B builds (scratch experiments): an alternative .so
+    LIB_PATH = Path(__import__("os").environ["FT_LIB_VARIANT"])
 
 
 class FractimeError(RuntimeError):

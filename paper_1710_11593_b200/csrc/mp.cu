@@ -364,6 +364,204 @@ __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
     }
 }
 
+// ---- persistent split K-branch levels (n = 32768, 65536) ----------------------
+// The three passes of a split level (fold, K branch transforms, combine) as ONE
+// persistent kernel fed by a task queue, per row pair instead of per batch: task
+// group g = { fold(g), branch(g - D, 0..K-1), combine(g - 2D) }.  A pair's folded
+// branch inputs / branch results live in ring slot p % RS of the scratch (RS >=
+// 2D + 1 pairs, ~50 MB: L2-resident, so the round trip no longer goes to HBM),
+// and every task waits (one thread, acquire loads) only for the tasks it reads:
+// branch(p, .) for fold(p); combine(p) for all K branches; fold(p) for the
+// combine that last used its slot.  Memory-bound folds / combines and the
+// FP64-bound branch FFTs of different pairs run side by side on every SM
+// instead of as separate full-GPU launches.  Scratch reads use ld.global.cg
+// (slots are rewritten during the kernel).
+struct SplitQ {
+    unsigned* ctr;  // [0] task counter; [1, 1+RS) folds done, [1+RS, 1+2RS) branches done,
+                    // [1+2RS, 1+3RS) combines done -- per slot, cumulative over the slot's uses
+    int RS, D, npairs, ntasks;
+    int probe;  // timing probes (wrong results): bit 0 skips branch work, bit 1 fold / combine work
+};
+
+__device__ __forceinline__ void spq_wait(const unsigned* c, unsigned target) {
+    if (threadIdx.x == 0) {
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void spq_signal_add(unsigned* c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(c, 1u);
+    }
+}
+__device__ __forceinline__ cplx ldcgc(const cplx* p) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    return {v.x, v.y};
+}
+
+constexpr int kSplitParts = 4;  // fold / combine tasks per pair (m / 4 points each; 2 and 8 measured
+                                // the same or slower, as were smem-staged cp.async variants)  // fold / combine tasks per pair (m / 4 points each: shorter tasks)
+
+template <int K, int LOGM>
+__global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, SplitQ q) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    __shared__ int s_task;
+    constexpr int m = 1 << LOGM;
+    constexpr int Q0 = m / 16;
+    const int n = a.n;
+    const uint64_t N = a.N;
+    const int RS = q.RS;
+    unsigned* fold_done = q.ctr + 1;
+    unsigned* br_done = q.ctr + 1 + RS;
+    unsigned* comb_done = q.ctr + 1 + 2 * RS;
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    for (;;) {
+        __syncthreads();  // previous task's shared state is dead
+        if (threadIdx.x == 0) s_task = (int)atomicAdd(q.ctr, 1u);
+        __syncthreads();
+        const int task = s_task;
+        if (task >= q.ntasks) return;
+        constexpr int NS = kSplitParts, GT = NS + K + NS;  // tasks per group
+        const int g = task / GT, r = task - g * GT;
+        const int p = r < NS ? g : r < NS + K ? g - q.D : g - 2 * q.D;
+        if (p < 0 || p >= q.npairs) continue;
+        const int slot = p % RS;
+        const unsigned use = (unsigned)(p / RS);
+        cplx* sc = a.scratch + (uint64_t)slot * K * m;
+        const int pb = p / a.pairs_per_problem, lp = p - pb * a.pairs_per_problem;
+        const int i1 = 2 * lp;
+        const bool has2 = i1 + 1 < a.nodes;
+        const uint64_t row1 = (uint64_t)(pb * a.nodes + i1);
+        if (r < NS) {
+            // ---- fold(p, part): f_b(rr) = theta_b^rr sum_q x_q(rr) zeta_b^q (mp_fold_kernel) ----
+            spq_wait(comb_done + slot, use * NS);  // the slot's previous pair is fully combined
+            const double* x1 = a.U + row1 * N + a.lo;
+#pragma unroll 1
+            for (int rr = r * (m / NS) + threadIdx.x; rr < (r + 1) * (m / NS) && !(q.probe & 2); rr += blockDim.x) {
+                cplx v[K];
+#pragma unroll
+                for (int qq = 0; qq < K / 2; ++qq) {
+                    v[qq].x = x1[(uint64_t)qq * m + rr];
+                    v[qq].y = has2 ? x1[N + (uint64_t)qq * m + rr] : 0.0;
+                }
+#pragma unroll
+                for (int qq = K / 2; qq < K; ++qq) v[qq] = {0.0, 0.0};
+                dft_reg<K, true>(v);
+                cplx* out = sc + rr;
+                out[0] = v[0];
+#pragma unroll
+                for (int bb = 1; bb < K; ++bb) out[(uint64_t)bb * m] = cmulc(v[bb], ldgc(&a.tw[n + bb * rr]));
+            }
+            spq_signal_add(fold_done + slot);
+        } else if (r < NS + K) {
+            // ---- branch(p, b): m-point transform, branch spectrum, inverse (mp_kernel<.., FOLDED>) ----
+            const int b = r - NS;
+            spq_wait(fold_done + slot, (use + 1u) * NS);
+            const cplx* in = sc + (uint64_t)b * m;  // folded and twisted by fold(p)
+            if (q.probe & 1) {  // timing probe: no branch work
+                spq_signal_add(br_done + slot);
+                continue;
+            }
+            for (int t = threadIdx.x; t < m / 16; t += blockDim.x) {
+                const int j = t;
+                cplx v[16];
+#pragma unroll
+                for (int pp = 0; pp < 16; ++pp) v[pp] = ldcgc(&in[j + pp * Q0]);
+                dft_reg<16, false>(v);
+                cplx w[16];
+                pass_twiddles<16>(w, a.tw, m, j);
+#pragma unroll
+                for (int qq = 1; qq < 16; ++qq) v[qq] = cmul(v[qq], w[qq]);
+                const int pbx = sphys(j);
+#pragma unroll
+                for (int qq = 0; qq < 16; ++qq) buf[pbx + qq * (Q0 + (Q0 >> 4))] = v[qq];
+            }
+            __syncthreads();
+            mid_fwd<LOGM - 4, LOGM>(buf, m, a.tw);
+            {
+                constexpr int RL = Plan1<LOGM>::RL;
+                for (int t = threadIdx.x; t < m / RL; t += blockDim.x) {
+                    const int base = t * RL;
+                    const int pbx = sphys(base);
+                    cplx v[RL];
+#pragma unroll
+                    for (int pp = 0; pp < RL; ++pp) v[pp] = buf[pbx + pp];
+                    dft_reg<RL, false>(v);
+                    const cplx* sp = a.spec + ((uint64_t)pb * K + b) * m + base;
+#pragma unroll
+                    for (int pp = 0; pp < RL; ++pp) v[pp] = cmul(v[pp], ldgc(&sp[pp]));
+                    dft_reg<RL, true>(v);
+#pragma unroll
+                    for (int pp = 0; pp < RL; ++pp) buf[pbx + pp] = v[pp];
+                }
+            }
+            __syncthreads();
+            mid_inv<LOGM - 4, LOGM>(buf, m, a.tw);
+            pass_c<16, LOGM, true>(buf, m, a.tw);
+            __syncthreads();
+            cplx* out = sc + (uint64_t)b * m;
+            for (int idx = threadIdx.x; idx < m; idx += blockDim.x) out[idx] = buf[sphys(idx)];
+            spq_signal_add(br_done + slot);
+        } else {
+            // ---- combine(p, part): untwist, K-point DFT, the K/2 target outputs (mpB_kernel) ----
+            const int part = r - NS - K;
+            spq_wait(br_done + slot, (use + 1u) * K);
+#pragma unroll 1
+            for (int rr = part * (m / NS) + threadIdx.x; rr < (part + 1) * (m / NS) && !(q.probe & 2); rr += blockDim.x) {
+                double r1[K / 2], r2[K / 2];
+#pragma unroll
+                for (int qq = 0; qq < K / 2; ++qq) {
+                    const uint64_t t = a.mid + (uint64_t)qq * m + rr;
+                    r1[qq] = (t < tend && a.rsrc) ? a.rsrc[row1 * N + t] : 0.0;
+                    r2[qq] = (t < tend && has2 && a.rsrc) ? a.rsrc[(row1 + 1) * N + t] : 0.0;
+                }
+                cplx wv[K];
+#pragma unroll
+                for (int bb = 0; bb < K; ++bb) wv[bb] = ldcgc(&sc[(uint64_t)bb * m + rr]);
+                const cplx w1 = ldgc(&a.tw[n + rr]);  // w_n^rr
+                cplx wp = w1;
+#pragma unroll
+                for (int bb = 1; bb < K; ++bb) {
+                    wv[bb] = cmul(wv[bb], wp);
+                    if (bb + 1 < K) wp = cmul(wp, w1);
+                }
+                dft_reg<K, false>(wv);
+#pragma unroll
+                for (int qq = K / 2; qq < K; ++qq) {
+                    const uint64_t t = a.mid + (uint64_t)(qq - K / 2) * m + rr;
+                    if (t >= tend) continue;
+                    cplx y = wv[qq];
+                    const int tp = (int)(t - a.mid);
+                    if (tp < a.J - 1) {
+                        const double* cp = a.col + (uint64_t)pb * N;
+                        const double* x1 = a.U + row1 * N;
+                        const uint64_t jlo = (t >= a.lo + (uint64_t)(a.J - 1)) ? t - (uint64_t)(a.J - 1) : a.lo;
+                        double s1 = 0.0, s2 = 0.0;
+                        for (uint64_t j = a.mid; j-- > jlo;) {
+                            const double cv = cp[t - j];
+                            s1 = fma(cv, x1[j], s1);
+                            if (has2) s2 = fma(cv, x1[N + j], s2);
+                        }
+                        y.x += s1;
+                        y.y += s2;
+                    }
+                    a.X[row1 * N + t] = r1[qq - K / 2] - y.x;
+                    if (has2) a.X[(row1 + 1) * N + t] = r2[qq - K / 2] - y.y;
+                }
+            }
+            spq_signal_add(comb_done + slot);
+        }
+    }
+}
+
 // ---- single-CTA n-point FFT history product (512 <= n <= 8192) -------------
 // One CTA transforms G row pairs of n = 2^LOGN points (the zero-padded source
 // block).  Passes (radix 16 from S = n down, remainder radix last):
@@ -933,8 +1131,57 @@ static uint64_t split_batch_bytes() {
     return b;
 }
 
+// persistent split level (mp_split_kernel): default; FT_SPLIT_BATCHED=1 is the A/B switch back
+// to the batched fold / branch / combine launches below
+static bool split_persistent() {
+    static const bool on = getenv("FT_SPLIT_BATCHED") == nullptr;
+    return on;
+}
+constexpr uint64_t kSplitCtrOffset = kMpScratchBytes - (64u << 10);  // queue counters: last 64 KB of the scratch
+
+template <int K, int LOGM>
+static cudaError_t launch_mp_split_persistent(const MpArgs& a, cudaStream_t st) {
+    constexpr int m = 1 << LOGM;
+    const size_t smem = mp_smem_bytes(1, m);
+    static DeviceOnce attr_set;
+    static int occ = 0, sms = 0;
+    if (attr_set.first()) {
+        cudaError_t e = cudaFuncSetAttribute(mp_split_kernel<K, LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mp_split_kernel<K, LOGM>, kMpThreads, smem);
+        if (e != cudaSuccess) return e;
+        attr_set.done();
+    }
+    const int ctas = sms * std::max(occ, 1);
+    SplitQ q;
+    q.npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    // lookahead: about twice the task groups the resident CTAs hold at once
+    static const int dknob = getenv("FT_SPLIT_D") ? atoi(getenv("FT_SPLIT_D")) : 0;  // tuning knob
+    q.D = dknob > 0 ? dknob : std::max(4, 2 * ctas / (K + 2 * kSplitParts) + 2);
+    // ring: pairs p - 2D .. p are live; fold(p) reuses the slot of pair p - RS, whose combine sits
+    // RS - 2D groups back -- give it D more groups so folds rarely wait on a running combine
+    static const int rknob = getenv("FT_SPLIT_RS") ? atoi(getenv("FT_SPLIT_RS")) : 0;  // tuning knob
+    q.RS = rknob > 0 ? rknob : 3 * q.D + 1;
+    if ((uint64_t)q.RS * K * m * sizeof(cplx) > kSplitCtrOffset) q.RS = (int)(kSplitCtrOffset / ((uint64_t)K * m * sizeof(cplx)));
+    if (q.RS < 2 * q.D + 1) q.D = (q.RS - 1) / 2;
+    q.ntasks = (q.npairs + 2 * q.D) * (K + 2 * kSplitParts);
+    static const int probe = getenv("FT_SPLIT_PROBE") ? atoi(getenv("FT_SPLIT_PROBE")) : 0;
+    q.probe = probe;
+    q.ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(a.scratch) + kSplitCtrOffset);
+    cudaError_t e = cudaMemsetAsync(q.ctr, 0, sizeof(unsigned) * (1 + 3 * (size_t)q.RS), st);
+    if (e != cudaSuccess) return e;
+    // co-residency is what makes the dependency waits safe (a waiting CTA only waits on tasks
+    // dequeued before its own): never more CTAs than fit at once
+    return launch_ex(mp_split_kernel<K, LOGM>, dim3(std::min(ctas, q.ntasks)), dim3(kMpThreads), smem, st, 1, a, q);
+}
+
 template <int K, int LOGM>
 static cudaError_t launch_mp_split(const MpArgs& a0, cudaStream_t st) {
+    if (split_persistent()) return launch_mp_split_persistent<K, LOGM>(a0, st);
     static DeviceOnce attr_set;
     if (attr_set.first()) {
         cudaFuncSetAttribute(mp_kernel<K, LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1065,7 +1312,7 @@ cudaError_t launch_spectra_single(const double* col, uint64_t N, int B, int n, i
 
 // Kernels launch_mp issues for this product (split levels: 2 or 3 per pair batch).
 int mp_kernel_count(const MpArgs& a) {
-    if (mp_is_single(a.n) || mp_is_direct(a.n) || !a.scratch) return 1;
+    if (mp_is_single(a.n) || mp_is_direct(a.n) || !a.scratch || split_persistent()) return 1;
     static const int prefold_min_k = getenv("FT_PREFOLD_MIN_K") ? atoi(getenv("FT_PREFOLD_MIN_K")) : 16;
     const bool prefold = a.K >= prefold_min_k && getenv("FT_NO_PREFOLD") == nullptr;
     const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
