@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kMpThreads) mp_fold_kernel(MpArgs a) {
     out[0] = v[0];
 #pragma unroll
     for (int bb = 1; bb < K; ++bb) out[(uint64_t)bb * m] = cmulc(v[bb], ldgc(&a.tw[n + bb * r]));
+    // (the persistent split kernel forms these twists from 4 coalesced loads, pass_twiddles)
 }
 
 // Cross-branch combine of the split K-branch levels: thread <-> (pair, r):
@@ -406,7 +407,10 @@ __device__ __forceinline__ cplx ldcgc(const cplx* p) {
     return {v.x, v.y};
 }
 
-constexpr int kSplitParts = 4;  // fold / combine tasks per pair (m / 4 points each; 2 and 8 measured
+#ifndef FT_SPLIT_PARTS
+#define FT_SPLIT_PARTS 4
+#endif
+constexpr int kSplitParts = FT_SPLIT_PARTS;  // fold / combine tasks per pair (m / 4 points each; 2 and 8 measured
                                 // the same or slower, as were smem-staged cp.async variants)  // fold / combine tasks per pair (m / 4 points each: shorter tasks)
 
 template <int K, int LOGM>
@@ -455,10 +459,14 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
 #pragma unroll
                 for (int qq = K / 2; qq < K; ++qq) v[qq] = {0.0, 0.0};
                 dft_reg<K, true>(v);
+                // twists theta_b^rr = w_n^(b rr), b < K: 4 coalesced table loads + products
+                // (pass_twiddles) instead of K-1 loads at stride b rr (uncoalesced, ncu)
+                cplx tw[K];
+                pass_twiddles<K>(tw, a.tw, n, rr);
                 cplx* out = sc + rr;
                 out[0] = v[0];
 #pragma unroll
-                for (int bb = 1; bb < K; ++bb) out[(uint64_t)bb * m] = cmulc(v[bb], ldgc(&a.tw[n + bb * rr]));
+                for (int bb = 1; bb < K; ++bb) out[(uint64_t)bb * m] = cmulc(v[bb], tw[bb]);
             }
             spq_signal_add(fold_done + slot);
         } else if (r < NS + K) {
@@ -526,13 +534,10 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
                 cplx wv[K];
 #pragma unroll
                 for (int bb = 0; bb < K; ++bb) wv[bb] = ldcgc(&sc[(uint64_t)bb * m + rr]);
-                const cplx w1 = ldgc(&a.tw[n + rr]);  // w_n^rr
-                cplx wp = w1;
+                cplx tw[K];  // untwists w_n^(b rr): 4 coalesced loads + products, shallow dependency chain
+                pass_twiddles<K>(tw, a.tw, n, rr);
 #pragma unroll
-                for (int bb = 1; bb < K; ++bb) {
-                    wv[bb] = cmul(wv[bb], wp);
-                    if (bb + 1 < K) wp = cmul(wp, w1);
-                }
+                for (int bb = 1; bb < K; ++bb) wv[bb] = cmul(wv[bb], tw[bb]);
                 dft_reg<K, false>(wv);
 #pragma unroll
                 for (int qq = K / 2; qq < K; ++qq) {
