@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(kMpThreads) mpB_kernel(MpArgs a) {
 // combine that last used its slot.  Memory-bound folds / combines and the
 // FP64-bound branch FFTs of different pairs run side by side on every SM
 // instead of as separate full-GPU launches.  Scratch reads use ld.global.cg
-// (slots are rewritten during the kernel).
+// (slots are rewritten during the kernel); the source and target streams are
+// marked evict-first (ld/st.global.cs) so they do not push the ring out of L2.
 struct SplitQ {
     unsigned* ctr;  // [0] task counter; [1, 1+RS) folds done, [1+RS, 1+2RS) branches done,
                     // [1+2RS, 1+3RS) combines done -- per slot, cumulative over the slot's uses
@@ -453,8 +454,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
                 cplx v[K];
 #pragma unroll
                 for (int qq = 0; qq < K / 2; ++qq) {
-                    v[qq].x = x1[(uint64_t)qq * m + rr];
-                    v[qq].y = has2 ? x1[N + (uint64_t)qq * m + rr] : 0.0;
+                    v[qq].x = __ldcs(x1 + (uint64_t)qq * m + rr);
+                    v[qq].y = has2 ? __ldcs(x1 + N + (uint64_t)qq * m + rr) : 0.0;
                 }
 #pragma unroll
                 for (int qq = K / 2; qq < K; ++qq) v[qq] = {0.0, 0.0};
@@ -528,8 +529,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
 #pragma unroll
                 for (int qq = 0; qq < K / 2; ++qq) {
                     const uint64_t t = a.mid + (uint64_t)qq * m + rr;
-                    r1[qq] = (t < tend && a.rsrc) ? a.rsrc[row1 * N + t] : 0.0;
-                    r2[qq] = (t < tend && has2 && a.rsrc) ? a.rsrc[(row1 + 1) * N + t] : 0.0;
+                    r1[qq] = (t < tend && a.rsrc) ? __ldcs(a.rsrc + row1 * N + t) : 0.0;
+                    r2[qq] = (t < tend && has2 && a.rsrc) ? __ldcs(a.rsrc + (row1 + 1) * N + t) : 0.0;
                 }
                 cplx wv[K];
 #pragma unroll
@@ -558,8 +559,8 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
                         y.x += s1;
                         y.y += s2;
                     }
-                    a.X[row1 * N + t] = r1[qq - K / 2] - y.x;
-                    if (has2) a.X[(row1 + 1) * N + t] = r2[qq - K / 2] - y.y;
+                    __stcs(a.X + row1 * N + t, r1[qq - K / 2] - y.x);
+                    if (has2) __stcs(a.X + (row1 + 1) * N + t, r2[qq - K / 2] - y.y);
                 }
             }
             spq_signal_add(comb_done + slot);
