@@ -55,13 +55,13 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-# DRAM bytes / algorithmic bytes of one history-product launch, measured with
-# ncu --set full on B200 (profiles/ncu_r01/kernels.json): direct kernel
-# (n <= 128: 0.67), group-private single-CTA FFT (256 <= n <= 4096: 0.81 at
-# n = 256, 0.90 at n = 512), 2- and 4-CTA clusters (n = 8192, 16384: 1.00),
-# split K-branch kernels + combine with the branch scratch round trip
-# (n >= 32768: 2.15 at K = 8; the pre-folded K = 16 level is taken equal).
-NCU_DRAM_OVER_ALG = {"direct": 0.67, "single": 0.86, "cluster": 1.00, "split": 2.15}
+# DRAM bytes / algorithmic bytes of the history-product launches of one config-4
+# solve, per kernel family, measured with ncu over every launch of the solve
+# (profiles/ncu_r02/fp64_dram_per_launch_cfg4.csv.gz, summarised in DESIGN.md §4):
+# direct n <= 128: 0.68, single-CTA FFT 256 <= n <= 4096: 0.92, 2-/4-CTA clusters
+# (n = 8192, 16384): 1.00, persistent split levels (n >= 32768, their scratch ring
+# partly spilling to DRAM): 2.71.
+NCU_DRAM_OVER_ALG = {"direct": 0.68, "single": 0.92, "cluster": 1.00, "split": 2.71}
 
 
 def mp_family(n: int) -> str:
