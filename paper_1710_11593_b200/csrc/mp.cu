@@ -382,7 +382,8 @@ struct SplitQ {
     unsigned* ctr;  // [0] task counter; [1, 1+RS) folds done, [1+RS, 1+2RS) branches done,
                     // [1+2RS, 1+3RS) combines done -- per slot, cumulative over the slot's uses
     int RS, D, npairs, ntasks;
-    int probe;  // timing probes (wrong results): bit 0 skips branch work, bit 1 fold / combine work
+    int probe;  // timing probes (wrong results): bit 0 skips branch work, bit 1 fold / combine work;
+                // bit 2 (A/B, results unchanged) keeps the ring lines instead of discarding them
 };
 
 __device__ __forceinline__ void spq_wait(const unsigned* c, unsigned target) {
@@ -540,6 +541,14 @@ __global__ void __launch_bounds__(kMpThreads, 2) mp_split_kernel(MpArgs a, Split
 #pragma unroll
                 for (int bb = 1; bb < K; ++bb) wv[bb] = cmul(wv[bb], tw[bb]);
                 dft_reg<K, false>(wv);
+                // the slot's branch results are dead once read: drop their L2 lines without the
+                // write-back (otherwise every ring write eventually costs a DRAM write, ncu)
+                __syncwarp();
+                if ((rr & 7) == 0 && !(q.probe & 4)) {
+#pragma unroll
+                    for (int bb = 0; bb < K; ++bb)
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(&sc[(uint64_t)bb * m + rr]) : "memory");
+                }
 #pragma unroll
                 for (int qq = K / 2; qq < K; ++qq) {
                     const uint64_t t = a.mid + (uint64_t)(qq - K / 2) * m + rr;

@@ -24,12 +24,12 @@ cap() {  # name kernel-regex launch-skip [prof args]
   gzip -c /tmp/ncu/cap_${name}_sass.csv > $O/cap_${name}_sass.csv.gz
 }
 cap leaf_fused "leaf_fused" 100
-cap split16 "mp_split_kernel<16" 0
-cap split8 "mp_split_kernel<8" 0
-cap cluster2 "mp_kernel<2" 0
-cap cluster4 "mp_kernel<4" 0
-cap mp1g9 "mp1g_kernel<9" 20
-cap mp1g12 "mp1g_kernel<12" 4
+cap split16 "mp_split_kernel<.int.16" 0
+cap split8 "mp_split_kernel<.int.8," 0
+cap cluster2 "mp_kernel<.int.2," 0
+cap cluster4 "mp_kernel<.int.4," 0
+cap mp1g9 "mp1g_kernel<.int.9>" 20
+cap mp1g12 "mp1g_kernel<.int.12>" 4
 cap direct64 "mp_direct_kernel" 300
 cap ode_whole "ode_whole_kernel" 0 --config 1
 cap leaf_cfg2 "leaf_kernel" 60 --config 2
