@@ -35,6 +35,11 @@
 namespace ftb {
 
 constexpr int kLeafUnroll = FT_LEAF_UNROLL;
+#ifndef FT_STAGE_U
+#define FT_STAGE_U 8
+#endif
+constexpr int kStageU = FT_STAGE_U;  // 16-byte loads in flight per thread staging a leaf tile
+                                     // (16: cfg4 +3 ms -- the 128 CTAs staging at once are HBM-bound)
 
 // in-leaf history weights col[1..L) of batched plans (B > 1), read through the
 // constant cache with a CTA-uniform index (measured: config 5 97.2 -> 92.3 ms vs
@@ -153,14 +158,14 @@ template <int L>
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, const double* radd, uint64_t row0,
                                            uint64_t N, uint64_t t0, int rows, int len) {
     // 16-byte loads when rows are 16-byte aligned and whole (the common case:
-    // even N, full leaf); 8 double2 in flight per thread
+    // even N, full leaf); kStageU double2 in flight per thread
     if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
         constexpr int HL = L / 2;
         const int total = rows * HL;
-        for (int e0 = 0; e0 < total; e0 += 8 * kLeafThreads) {
-            double2 v[8];
+        for (int e0 = 0; e0 < total; e0 += kStageU * kLeafThreads) {
+            double2 v[kStageU];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kStageU; ++u) {
                 const int e = e0 + u * kLeafThreads + threadIdx.x;
                 const int q = e / HL, k2 = e - q * HL;
                 v[u] = (e < total && src) ? __ldcg(reinterpret_cast<const double2*>(src + (row0 + q) * N + t0) + k2)
@@ -168,7 +173,7 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
             }
             if (radd) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < kStageU; ++u) {
                     const int e = e0 + u * kLeafThreads + threadIdx.x;
                     const int q = e / HL, k2 = e - q * HL;
                     if (e < total) {
@@ -179,7 +184,7 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kStageU; ++u) {
                 const int e = e0 + u * kLeafThreads + threadIdx.x;
                 const int q = e / HL, k2 = e - q * HL;
                 if (e < total) {
