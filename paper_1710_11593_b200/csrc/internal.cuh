@@ -31,11 +31,11 @@ struct ProblemConst {
 
 constexpr int kLeafThreads = 256;
 constexpr uint64_t kMaxTimeSteps = 65536;  // N limit (FT_ELENGTH): history products up to n = 65536
-// LeafArgs::kc layout (single-problem plans): in-leaf weights col[0..32), then
-// the uniform scan multipliers lam^(NPT 2^d) (d < 5), lam^(32 NPT), lam,
-// lam^(v+1) and lam^(NPT-v) (v < 8).
-constexpr int kKcPow = 32, kKcLamW = 37, kKcLam = 38, kKcV1 = 40, kKcNv = 48, kKcCol2 = 56, kKcLen = 88;
-// (kKcCol2: col[32..64), the far half of the level-0 history window fused into the leaf)
+// LeafArgs::kc layout (single-problem plans): col[0..64) (the in-leaf weights, lags < 32,
+// and the far half of the level-0 history window fused into the leaf, contiguous so the
+// rolled product indexes them at a runtime offset), then the uniform scan multipliers
+// lam^(NPT 2^d) (d < 5), lam^(32 NPT), lam, lam^(v+1) and lam^(NPT-v) (v < 8).
+constexpr int kKcCol2 = 32, kKcPow = 64, kKcLamW = 69, kKcLam = 70, kKcV1 = 72, kKcNv = 80, kKcLen = 88;
 constexpr int kMaxSlabs = 160;
 constexpr int kMaxLeafProblems = 128;  // problems per plan
 constexpr int kMpThreads = 256;

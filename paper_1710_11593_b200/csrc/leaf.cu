@@ -154,12 +154,14 @@ struct LeafConsts<true, NPT, L> {
 // consecutive threads read consecutive steps of a node row, 8 loads in flight.
 // radd (optional, same layout as src): added element-wise -- the streamed host
 // path keeps the caller's R out of X until the leaf that solves those steps.
-template <int L>
+template <int L, bool LEAN = false>
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, const double* radd, uint64_t row0,
                                            uint64_t N, uint64_t t0, int rows, int len) {
     // 16-byte loads when rows are 16-byte aligned and whole (the common case:
-    // even N, full leaf); kStageU double2 in flight per thread
-    if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
+    // even N, full leaf); kStageU double2 in flight per thread.  LEAN (host-checked:
+    // even N, full leaves, no radd): only this path is compiled.
+    if (LEAN) radd = nullptr;
+    if (LEAN || (len == L && (N & 1) == 0 && (t0 & 1) == 0)) {
         constexpr int HL = L / 2;
         const int total = rows * HL;
         for (int e0 = 0; e0 < total; e0 += kStageU * kLeafThreads) {
@@ -215,10 +217,10 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
 }
 
 // X[row0 + q][t0 + k] = src[q][k] (row stride L+1), 16-byte stores when aligned
-template <int L>
+template <int L, bool LEAN = false>
 __device__ __forceinline__ void store_rows(double* X, const double* src, uint64_t row0, uint64_t N, uint64_t t0,
                                            int rows, int len, int tid, int nth) {
-    if (len == L && (N & 1) == 0 && (t0 & 1) == 0) {
+    if (LEAN || (len == L && (N & 1) == 0 && (t0 & 1) == 0)) {
         constexpr int HL = L / 2;
         for (int e = tid; e < rows * HL; e += nth) {
             const int q = e / HL, k2 = e - q * HL;
@@ -324,7 +326,11 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
 // MODE 1 (LOCAL): phase 1 of the slab decomposition (zero inter-slab carries);
 //   per step the slab's exported carries (F at its last node, B at its first)
 //   are written to xch[cta][k][2].
-template <int KIND, int NPT, int L, int MODE, bool PC = false>
+// LEAN (host-checked in launch_fused_t: even N, full leaf, no radd / fused RHS / Scheme-2
+// stencil): the generic staging, forcing and V paths are compiled out.  The slab leaf's code
+// must stay inside the SM's 64 KB of instruction cache: ncu showed every instruction past
+// that mark stalling on instruction fetch (30 % of the leaf's warp samples at 150 KB).
+template <int KIND, int NPT, int L, int MODE, bool PC = false, bool LEAN = false>
 __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x) {
     // s_out: [slab nodes][L + 1] solution tile (stays resident for the fused leaf)
     __shared__ double s_wt[2][32][2];
@@ -342,7 +348,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     const uint64_t N = a.N;
     const double* colp = a.col + (uint64_t)pb * N;
     const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
-    const int len = a.len;
+    const int len = LEAN ? L : a.len;
 
     (void)colp;
 
@@ -352,7 +358,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     if (stamp) a.dbg_clk[8] = clock64();
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
-    stage_rows<L>(s_out, a.src, a.radd, rowb, N, a.t0, mreal, len);
+    stage_rows<L, LEAN>(s_out, a.src, a.radd, rowb, N, a.t0, mreal, len);
     __syncthreads();
     if (stamp) a.dbg_clk[15] = clock64();
     double tile[NPT][L];
@@ -367,41 +373,52 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         if (a.fuse0) {
             // level-0 history product (n = 64) of the previous leaf onto this one:
             // tile[v][k] -= sum_j col[32 + k - j] U[row][t0 - 32 + j] (lags 1..63), with the
-            // previous leaf's U staged through s_out (free until the step loop writes it)
+            // previous leaf's U staged through s_out (free until the step loop writes it).
+            // Rolled over output chunks (instruction footprint): the weights are constant-bank
+            // operands at a CTA-uniform runtime offset (kc[0 .. 2L) holds lags 0 .. 2L-1), each
+            // chunk's sums go back to the thread's own row of s_out and are subtracted from the
+            // register window afterwards.
             __syncthreads();
-            stage_rows<L>(s_out, a.X, nullptr, rowb, N, a.t0 - L, mreal, L);
+            stage_rows<L, LEAN>(s_out, a.X, nullptr, rowb, N, a.t0 - L, mreal, L);
             __syncthreads();
             if (stamp) a.dbg_clk[5] = clock64();
-#pragma unroll
+#pragma unroll 1
             for (int v = 0; v < NPT; ++v) {
                 const int q = tid * NPT + v;
                 if (q >= mreal) continue;
+                double* row = s_out + q * (L + 1);
                 double u[L];
 #pragma unroll
-                for (int jj = 0; jj < L; ++jj) u[jj] = s_out[q * (L + 1) + jj];
-                // 8 outputs at a time: each output still sums jj ascending (bitwise equal to
-                // the standalone direct product) with 8 independent FMA chains in flight
-#pragma unroll
+                for (int jj = 0; jj < L; ++jj) u[jj] = row[jj];
+                // 8 outputs at a time: each output sums jj ascending (bitwise equal to the
+                // standalone direct product) with 8 independent FMA chains in flight
+#pragma unroll 1
                 for (int k0 = 0; k0 < L; k0 += 8) {
+                    const double* wp = a.kc + L + k0;  // wp[kk - jj]: weight of lag L + k0 + kk - jj
                     double acc[8];
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
 #pragma unroll
                     for (int jj = 0; jj < L; ++jj) {
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const int lag = L + k0 + kk - jj;  // 1 .. 2L-1
-                            const double c = lag < L ? a.kc[lag] : a.kc[kKcCol2 + lag - L];
-                            acc[kk] = fma(c, u[jj], acc[kk]);
-                        }
+                        for (int kk = 0; kk < 8; ++kk) acc[kk] = fma(wp[kk - jj], u[jj], acc[kk]);
                     }
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) tile[v][k0 + kk] -= acc[kk];
+                    for (int kk = 0; kk < 8; ++kk) row[k0 + kk] = acc[kk];
+                }
+            }
+            // (own rows only: no barrier)
+#pragma unroll
+            for (int v = 0; v < NPT; ++v) {
+                const int q = tid * NPT + v;
+                if (q < mreal) {
+#pragma unroll
+                    for (int k = 0; k < L; ++k) tile[v][k] -= s_out[q * (L + 1) + k];
                 }
             }
         }
     }
-    if (a.genA) {
+    if (!LEAN && a.genA) {
         // fused separable RHS (ft_solve_fast_modes): tile += sum_j A[row][j] T[pb][t][j]
         // straight into the register window; T is warp-uniform (broadcast loads)
         const int J = a.genJ;
@@ -501,7 +518,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         double xs[NPT];
 #pragma unroll
         for (int v = 0; v < NPT; ++v)  // (compile-time false for the tridiagonal operator: x stays on the fast path)
-            xs[v] = (KIND == SK_UPWIND && a.stencil) ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
+            xs[v] = (KIND == SK_UPWIND && !LEAN && a.stencil) ? x[v] + (v > 0 ? x[v - 1] : xleft) : x[v];
         // push x_k into the remaining in-leaf steps; chunks whose first entry lies past
         // the leaf end (k + 1 + c >= len) are dead and skipped (one warp-uniform test per chunk)
 #pragma unroll
@@ -521,8 +538,8 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     __syncthreads();
     if (stamp) a.dbg_clk[10] = clock64();
     // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
-    if (write_x) store_rows<L>(a.X, s_out, rowb, N, a.t0, mreal, len, tid, blockDim.x);
-    if (MODE == 0 && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1) (single-slab problems)
+    if (write_x) store_rows<L, LEAN>(a.X, s_out, rowb, N, a.t0, mreal, len, tid, blockDim.x);
+    if (!LEAN && MODE == 0 && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1) (single-slab problems)
         for (int e = tid; e < mreal * len; e += blockDim.x) {
             const int q = e / len, k = e - q * len;
             const double up = q > 0 ? s_out[(q - 1) * (L + 1) + k] : 0.0;
@@ -688,7 +705,7 @@ __global__ void __launch_bounds__(kMaxSlabs / 32 * 32 + 32) leaf_wbuild(LeafArgs
 // own slab over them, and a butterfly reduce-scatter + cross-warp sum folds
 // the 256 partial vectors (fixed order: bitwise reproducible, independent of
 // how slabs are partitioned over ranks).
-template <int KIND, int NPT, int L>
+template <int KIND, int NPT, int L, bool LEAN = false>
 __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, double* s_x, bool x_resident) {
     // s_c0: carries of every slab transposed to [L][2P + 1]; s_x: [m][L+1] phase-1 solution tile
     __shared__ double s_inj[L][2];          // this slab's EL_k, ER_k
@@ -699,7 +716,7 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int P = a.P;
-    const int len = a.len;
+    const int len = LEAN ? L : a.len;
     const int m = a.slab;
     const int JS = 2 * P + 1;
 
@@ -763,14 +780,22 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     if (stamp) a.dbg_clk[1] = clock64();
 
     // ---- phase 2: EL/ER_k = sum_{l<=k} sum_j W[k-l][j] c_l[j] ----
+    // One side at a time (rolled: instruction footprint, see leaf_body): every thread owns
+    // source carries j and accumulates the L injections of its slab over them; a butterfly
+    // reduce-scatter (lane keeps output `lane`) + cross-warp sum folds the partial vectors
+    // (fixed order: bitwise reproducible, independent of the rank partition).
     if (!(a.dbg & 1)) {
-        double acc[2 * L];  // [side][k]
-#pragma unroll
-        for (int o = 0; o < 2 * L; ++o) acc[o] = 0.0;
         const double* Ws = a.resp_w + ((uint64_t)pb * P + s) * 2 * L * 2 * P;
-        for (int j = tid; j < 2 * P; j += kLeafThreads) {
+        if (!TRI) {
+            for (int i = tid; i < (kLeafThreads / 32) * L; i += kLeafThreads) s_red[i / L][L + (i & (L - 1))] = 0.0;
+        }
+#pragma unroll 1
+        for (int side = 0; side < (TRI ? 2 : 1); ++side) {
+            double acc[L];
 #pragma unroll
-            for (int side = 0; side < (TRI ? 2 : 1); ++side) {
+            for (int o = 0; o < L; ++o) acc[o] = 0.0;
+#pragma unroll 1
+            for (int j = tid; j < 2 * P; j += kLeafThreads) {
                 double wv[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) wv[l] = __ldg(&Ws[((uint64_t)side * L + l) * 2 * P + j]);
@@ -778,24 +803,22 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
                 for (int l = 0; l < L; ++l) {
                     const double cv = l < len ? s_c0[l * JS + j] : 0.0;
 #pragma unroll
-                    for (int k = l; k < L; ++k) acc[side * L + k] = fma(wv[k - l], cv, acc[side * L + k]);
+                    for (int k = l; k < L; ++k) acc[k] = fma(wv[k - l], cv, acc[k]);
                 }
             }
-        }
-        // butterfly reduce-scatter over the warp: lane keeps outputs 2 lane, 2 lane + 1
 #pragma unroll
-        for (int st = 0; st < 5; ++st) {
-            const int off = 16 >> st, half = L >> st;
-            const bool up = (lane & off) != 0;
+            for (int st = 0; st < 5; ++st) {
+                const int off = 16 >> st, half = (L / 2) >> st;
+                const bool up = (lane & off) != 0;
 #pragma unroll
-            for (int i = 0; i < half; ++i) {
-                const double send = up ? acc[i] : acc[i + half];
-                const double keep = up ? acc[i + half] : acc[i];
-                acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                for (int i = 0; i < half; ++i) {
+                    const double send = up ? acc[i] : acc[i + half];
+                    const double keep = up ? acc[i + half] : acc[i];
+                    acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
             }
+            s_red[w][side * L + lane] = acc[0];
         }
-        s_red[w][2 * lane] = acc[0];
-        s_red[w][2 * lane + 1] = acc[1];
         __syncthreads();
         if (tid < 2 * L) {
             double v = 0.0;
@@ -810,34 +833,42 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
 
     if (stamp) a.dbg_clk[2] = clock64();
     // ---- phase 3: x = x0 + sum_l GL(l) EL_(k-l) + GR(l) ER_(k-l) ----
+    // Rolled: win[i] collects the responses to the injections of step st at step st + i; the
+    // finished correction of step st leaves at win[0].  Segments of 4 steps with a static
+    // window length (entries that would land past the leaf end are never formed).
     const int tsel = (s == P - 1) ? 1 : 0;
     // tables are time-major [side][l][q]: lanes (consecutive q) read coalesced
     const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
-    for (int q = tid; q < mreal; q += blockDim.x) {
-        double corr[L];
-#pragma unroll
-        for (int k = 0; k < L; ++k) corr[k] = 0.0;
 #pragma unroll 1
-        for (int side = 0; side < (TRI ? 2 : 1); ++side) {
-            double gv[L], inj[L];
+    for (int q = tid; q < mreal; q += blockDim.x) {
+        double gL[L], gR[TRI ? L : 1], win[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                gv[l] = GT[((uint64_t)side * L + l) * m + q];
-                inj[l] = s_inj[l][side];
-            }
-#pragma unroll
-            for (int k = 0; k < L; ++k)
-#pragma unroll
-                for (int l = 0; l <= k; ++l) corr[k] = fma(gv[l], inj[k - l], corr[k]);
+        for (int l = 0; l < L; ++l) {
+            gL[l] = GT[(uint64_t)l * m + q];
+            if (TRI) gR[l] = GT[((uint64_t)L + l) * m + q];
+            win[l] = 0.0;
         }
         double* xq = s_x + q * (L + 1);
 #pragma unroll
-        for (int k = 0; k < L; ++k) xq[k] += corr[k];
+        for (int sg = 0; sg < L / 4; ++sg) {
+            constexpr int dummy = 0;
+            (void)dummy;
+#pragma unroll 1
+            for (int st = 4 * sg; st < 4 * sg + 4; ++st) {
+                if (st >= len) break;
+                const double el = s_inj[st][0];
+                const double er = TRI ? s_inj[st][1] : 0.0;
+                xq[st] += fma(gL[0], el, TRI ? fma(gR[0], er, win[0]) : win[0]);
+#pragma unroll
+                for (int i = 0; i < L - 1 - 4 * sg; ++i)  // targets st + 1 + i <= L - 1
+                    win[i] = fma(gL[i + 1], el, TRI ? fma(gR[TRI ? i + 1 : 0], er, win[i + 1]) : win[i + 1]);
+            }
+        }
     }
     __syncthreads();
     if (stamp) a.dbg_clk[3] = clock64();
-    store_rows<L>(a.X, s_x, rowb, a.N, a.t0, mreal, len, tid, blockDim.x);
-    if (a.V) {  // Scheme 2 product sources V = U_i + U_(i-1); the slab's left neighbour value is EL
+    store_rows<L, LEAN>(a.X, s_x, rowb, a.N, a.t0, mreal, len, tid, blockDim.x);
+    if (!LEAN && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1); the slab's left neighbour value is EL
         for (int e = tid; e < mreal * len; e += blockDim.x) {
             const int q = e / len, k = e - q * len;
             const double left = q > 0 ? s_x[(q - 1) * (L + 1) + k] : s_inj[k][0];
@@ -881,7 +912,7 @@ __device__ __forceinline__ void prefetch_correct_tables(const LeafArgs& a) {
 
 // Single-GPU slab leaf in ONE cooperative kernel: phase 1, publish carries, a
 // grid barrier (all slabs co-resident), phases 2 + 3 on the resident tile.
-template <int KIND, int NPT, int L, bool PC>
+template <int KIND, int NPT, int L, bool PC, bool LEAN>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     extern __shared__ __align__(16) double s_dyn[];
     double* s_c0 = s_dyn;
@@ -889,7 +920,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
     if (stamp) a.dbg_clk[12] = clock64();
     prefetch_correct_tables<L>(a);
-    leaf_body<KIND, NPT, L, 1, PC>(a, s_x, false);
+    leaf_body<KIND, NPT, L, 1, PC, LEAN>(a, s_x, false);
     __syncthreads();
     if (stamp) a.dbg_clk[14] = clock64();
     if (threadIdx.x == 0) {
@@ -902,7 +933,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     }
     __syncthreads();
     if (stamp) a.dbg_clk[13] = clock64();
-    correct_body<KIND, NPT, L>(a, s_c0, s_x, true);
+    correct_body<KIND, NPT, L, LEAN>(a, s_c0, s_x, true);
 }
 
 // Partitioned slab leaf with the carry exchange done by the kernel itself over
@@ -993,13 +1024,18 @@ template <int KIND, int NPT, int L>
 static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
     static DeviceOnce attr;
+    const int mx = (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1)));
     if (attr.first()) {
-        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
-        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(leaf_fused<KIND, NPT, L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr.done();
     }
+    // the common case (whole leaves of an even-N problem, R from an array) runs the lean
+    // instantiation: generic staging / streamed-R / fused-RHS / Scheme-2 paths compiled out
+    static const bool no_lean = getenv("FT_NO_LEAN") != nullptr;
+    const bool lean = !no_lean && a.len == L && (a.N & 1) == 0 && !a.radd && !a.genA && !a.V && !a.stencil;
     // cooperative attribute through cudaLaunchKernelEx: capturable into the solve's CUDA graph
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
@@ -1011,8 +1047,11 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
     coop[0].val.cooperative = 1;
     cfg.attrs = coop;
     cfg.numAttrs = 1;
-    return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, true>, a)
-                      : cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, false>, a);
+    if (lean)
+        return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, true, true>, a)
+                          : cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, false, true>, a);
+    return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, true, false>, a)
+                      : cudaLaunchKernelEx(&cfg, leaf_fused<KIND, NPT, L, false, false>, a);
 }
 
 template <int KIND, int NPT, int L>
