@@ -167,7 +167,7 @@ int ft_plan_get_info(const ft_plan* plan, ft_plan_info* info);
  * the caller's collective: `exchange(user, count, stream)` must all-gather
  * `count` doubles per rank from every rank's send buffer into the recv buffer
  * (rank-major), ordered on `stream` -- e.g. ncclAllGather on that stream.  The
- * send/recv device buffers are registered with ft_set_exchange. */
+ * send/recv device buffers (16-byte aligned) are registered with ft_set_exchange. */
 typedef int (*ft_exchange_fn)(void* user, uint64_t count_per_rank, void* cuda_stream);
 int ft_setup_partitioned(const ft_problem* problem, const ft_options* options, int rank, int world,
                          ft_plan** out);

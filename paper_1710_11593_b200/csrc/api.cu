@@ -1029,6 +1029,8 @@ int ft_p2p_connect(ft_plan* p, const void* handles) {
 int ft_set_exchange(ft_plan* p, ft_exchange_fn fn, void* user, double* send_device, double* recv_device) {
     if (!p || !fn || !send_device || !recv_device) return set_err(FT_EINVAL, "ft_set_exchange: null argument");
     if (p->part_world <= 1) return set_err(FT_EINVAL, "ft_set_exchange: plan is not partitioned");
+    if ((reinterpret_cast<uintptr_t>(send_device) | reinterpret_cast<uintptr_t>(recv_device)) & 15)
+        return set_err(FT_EINVAL, "ft_set_exchange: carry buffers must be 16-byte aligned");
     p->exchange = fn;
     p->exchange_user = user;
     p->xsend_d = send_device;

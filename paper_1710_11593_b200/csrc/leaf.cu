@@ -724,19 +724,24 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     if (stamp) a.dbg_clk[0] = clock64();
     // load the carries of every slab of this problem (transposed) and the phase-1 tile
     const double* xin = a.xch + (uint64_t)pb * P * L * 2;
-    for (int i0 = 0; i0 < P * L * 2; i0 += 8 * kLeafThreads) {  // 8 loads in flight per thread
-        double v[8];
+    {   // 16-byte loads (one step's two carries of a slab), 16 in flight per thread
+        const double2* xin2 = reinterpret_cast<const double2*>(xin);
+        const int total2 = P * L;
+        for (int i0 = 0; i0 < total2; i0 += 16 * kLeafThreads) {
+            double2 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * kLeafThreads + tid;
-            v[u] = i < P * L * 2 ? __ldcg(&xin[i]) : 0.0;
-        }
+            for (int u = 0; u < 16; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                v[u] = i < total2 ? __ldcg(&xin2[i]) : make_double2(0.0, 0.0);
+            }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * kLeafThreads + tid;
-            if (i < P * L * 2) {
-                const int sp = i / (2 * L), r = i - sp * 2 * L;  // r = 2 l + side
-                s_c0[(r >> 1) * JS + 2 * sp + (r & 1)] = v[u];
+            for (int u = 0; u < 16; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                if (i < total2) {
+                    const int sp = i / L, l = i - sp * L;
+                    s_c0[l * JS + 2 * sp] = v[u].x;
+                    s_c0[l * JS + 2 * sp + 1] = v[u].y;
+                }
             }
         }
     }
@@ -859,9 +864,17 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
                 const double el = s_inj[st][0];
                 const double er = TRI ? s_inj[st][1] : 0.0;
                 xq[st] += fma(gL[0], el, TRI ? fma(gR[0], er, win[0]) : win[0]);
+                // targets st + 1 + i <= L - 1; blocks of 8 so that the two dependent products of an
+                // entry are 8 independent DFMAs apart (back to back they exposed the pipe latency)
 #pragma unroll
-                for (int i = 0; i < L - 1 - 4 * sg; ++i)  // targets st + 1 + i <= L - 1
-                    win[i] = fma(gL[i + 1], el, TRI ? fma(gR[TRI ? i + 1 : 0], er, win[i + 1]) : win[i + 1]);
+                for (int i0 = 0; i0 < L - 1 - 4 * sg; i0 += 8) {
+                    double t8[8];
+#pragma unroll
+                    for (int i = i0; i < i0 + 8 && i < L - 1 - 4 * sg; ++i)
+                        t8[i - i0] = TRI ? fma(gR[TRI ? i + 1 : 0], er, win[i + 1]) : win[i + 1];
+#pragma unroll
+                    for (int i = i0; i < i0 + 8 && i < L - 1 - 4 * sg; ++i) win[i] = fma(gL[i + 1], el, t8[i - i0]);
+                }
             }
         }
     }
