@@ -597,7 +597,8 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     if ((rc = alloc_copy((void**)&p->dbgclk_d, nullptr, sizeof(long long) * 16))) return rc;
     if (p->stencil && (rc = alloc_copy((void**)&p->vsrc_d, nullptr, sizeof(double) * rows_of(p) * N))) return rc;
     if (p->multi) {
-        if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * B * p->P * p->L))) return rc;
+        // (twice the carries of one leaf: the leaf-pair kernel double-buffers them)
+        if ((rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * 2 * B * p->P * p->L))) return rc;
         p->xsend_d = p->xch_d;
         if ((rc = alloc_copy((void**)&p->bar_d, nullptr, sizeof(unsigned)))) return rc;
         {
@@ -749,6 +750,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.stencil = p->stencil ? 1 : 0;
             const bool defer = io && io->defer;
             a.src = (op.first && !defer) ? rhs : X;
+            a.src2 = nullptr;
             a.radd = defer ? io->rdev : nullptr;
             a.fuse0 = (fuse0 && pend0) ? 1 : 0;
             if (a.fuse0 && pend0_first) a.src = rhs;  // the skipped product was this tile's first touch
@@ -797,6 +799,23 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.p2p_world = p->part_world;
             a.p2p_leaf = (int)leaf_index - 1;
             a.p2p_leaves = leaves_total;
+            // leaves 2i and 2i+1 with only the (folded) level-0 product between them: one kernel
+            bool pair = false;
+            if (fuse0 && !a.fuse0 && !p->p2p && p->multi && p->part_world == 1 && p->fused_leaf &&
+                oi + 2 < p->ops.size() && p->ops[oi + 1].kind != OP_LEAF && p->ops[oi + 1].level == 0 &&
+                p->ops[oi + 2].kind == OP_LEAF && p->ops[oi + 2].len == p->L && leaf_pair_ok(a, p->L)) {
+                a.src2 = p->ops[oi + 1].first ? rhs : X;  // the folded product was that tile's first touch
+                pair = true;
+            }
+            if (pair) {
+                FT_CUDA(launch_leaf_pair(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
+                ++leaf_index;
+                if (evs) {  // per-op timing: the pair's time is charged to its first leaf
+                    FT_CUDA(cudaEventRecord((*evs)[oi + 1], st));
+                    FT_CUDA(cudaEventRecord((*evs)[oi + 2], st));
+                }
+                oi += 2;
+            } else
             if (p->p2p) {  // exchange inside the kernel over peer memory: no hook, no second kernel
                 a.xch = reinterpret_cast<double*>((char*)p->p2p_block + kP2pHeader) +
                         (size_t)(a.p2p_leaf & 1) * p->P * p->L * 2;

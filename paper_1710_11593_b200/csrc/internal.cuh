@@ -129,6 +129,7 @@ inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
 struct LeafArgs {
     double* X;                 // rows x N, node-major (U for solved steps, R after)
     const double* src;         // where this leaf's R tile is read from (X or the caller's rhs)
+    const double* src2;        // leaf-pair kernel: the same for the second leaf of the pair
     const double* radd;        // streamed host solves: R added at staging (history in src), else null
     uint64_t N;                // row pitch = time steps
     uint64_t t0;               // first step of the leaf
@@ -237,6 +238,8 @@ cudaError_t launch_leaf(int kind, int npt, int L, bool multi, const LeafArgs& a,
 cudaError_t launch_leaf_correct(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double* W, cudaStream_t st);
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+bool leaf_pair_ok(const LeafArgs& a, int L);
+cudaError_t launch_leaf_pair(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st);
 // exchange block layout: [0] uint64 arrival counter, [8] uint32 solve epoch, [64..) receive

@@ -154,9 +154,11 @@ struct LeafConsts<true, NPT, L> {
 // consecutive threads read consecutive steps of a node row, 8 loads in flight.
 // radd (optional, same layout as src): added element-wise -- the streamed host
 // path keeps the caller's R out of X until the leaf that solves those steps.
+// sub (vector path only): dst holds values to subtract -- dst = src - dst (the leaf-pair
+// kernel leaves the level-0 history product of the previous leaf there).
 template <int L, bool LEAN = false>
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, const double* radd, uint64_t row0,
-                                           uint64_t N, uint64_t t0, int rows, int len) {
+                                           uint64_t N, uint64_t t0, int rows, int len, bool sub = false) {
     // 16-byte loads when rows are 16-byte aligned and whole (the common case:
     // even N, full leaf); kStageU double2 in flight per thread.  LEAN (host-checked:
     // even N, full leaves, no radd): only this path is compiled.
@@ -190,8 +192,14 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, const
                 const int e = e0 + u * kLeafThreads + threadIdx.x;
                 const int q = e / HL, k2 = e - q * HL;
                 if (e < total) {
-                    dst[q * (L + 1) + 2 * k2] = v[u].x;
-                    dst[q * (L + 1) + 2 * k2 + 1] = v[u].y;
+                    double* d = dst + q * (L + 1) + 2 * k2;
+                    if (sub) {
+                        d[0] = v[u].x - d[0];
+                        d[1] = v[u].y - d[1];
+                    } else {
+                        d[0] = v[u].x;
+                        d[1] = v[u].y;
+                    }
                 }
             }
         }
@@ -321,6 +329,40 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
     }
 }
 
+// Level-0 history product (n = 64) of the previous leaf onto the next one, per node row of
+// the calling thread: row[k] := sum_j col[32 + k - j] row[j] (lags 1..63), in place in the
+// thread's own rows of s_out (which hold the previous leaf's U).  Rolled over output chunks
+// (instruction footprint): the weights are constant-bank operands at a CTA-uniform runtime
+// offset (kc[0 .. 2L) holds lags 0 .. 2L-1).
+template <int NPT, int L>
+__device__ __forceinline__ void level0_rows(const LeafArgs& a, double* s_out, int tid, int mreal) {
+#pragma unroll 1
+    for (int v = 0; v < NPT; ++v) {
+        const int q = tid * NPT + v;
+        if (q >= mreal) continue;
+        double* row = s_out + q * (L + 1);
+        double u[L];
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) u[jj] = row[jj];
+        // 8 outputs at a time: each output sums jj ascending (bitwise equal to the
+        // standalone direct product) with 8 independent FMA chains in flight
+#pragma unroll 1
+        for (int k0 = 0; k0 < L; k0 += 8) {
+            const double* wp = a.kc + L + k0;  // wp[kk - jj]: weight of lag L + k0 + kk - jj
+            double acc[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < L; ++jj) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) acc[kk] = fma(wp[kk - jj], u[jj], acc[kk]);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) row[k0 + kk] = acc[kk];
+        }
+    }
+}
+
 // MODE 0 (SINGLE): the CTA spans the whole problem; the Dirichlet correction
 //   x += kF_i F_M + kB_i B_1 (host-precomputed per node) makes the step exact.
 // MODE 1 (LOCAL): phase 1 of the slab decomposition (zero inter-slab carries);
@@ -330,8 +372,10 @@ __device__ __forceinline__ void cta_scan(const double (&in)[NPT], const SC& sc,
 // stencil): the generic staging, forcing and V paths are compiled out.  The slab leaf's code
 // must stay inside the SM's 64 KB of instruction cache: ncu showed every instruction past
 // that mark stalling on instruction fetch (30 % of the leaf's warp samples at 150 KB).
-template <int KIND, int NPT, int L, int MODE, bool PC = false, bool LEAN = false>
-__device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x) {
+// PAIR (leaf_pair kernel): half = 1 is the second leaf of a pair whose first leaf's solution
+// is still in s_out: the level-0 product is formed there and the staged R subtracts it.
+template <int KIND, int NPT, int L, int MODE, bool PC = false, bool LEAN = false, bool PAIR = false>
+__device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x, int half = 0) {
     // s_out: [slab nodes][L + 1] solution tile (stays resident for the fused leaf)
     __shared__ double s_wt[2][32][2];
     __shared__ double s_own[2];
@@ -349,16 +393,23 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     const double* colp = a.col + (uint64_t)pb * N;
     const double* lp = a.lampow + (uint64_t)pb * a.lp_stride;
     const int len = LEAN ? L : a.len;
+    const uint64_t t0 = a.t0 + (PAIR ? (uint64_t)half * L : 0);
 
     (void)colp;
 
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
     const LeafConsts<PC, NPT, L> sc(a, pb, lp, pc.lam, lane);  // plan constants: before the dependency wait
-    pdl_wait();
+    if (!PAIR || half == 0) pdl_wait();
     if (stamp) a.dbg_clk[8] = clock64();
+    if (PAIR && half) {
+        __syncthreads();  // the store of the first leaf's solution has read every row
+        level0_rows<NPT, L>(a, s_out, tid, mreal);
+        __syncthreads();
+        if (stamp) a.dbg_clk[5] = clock64();
+    }
     // input tile: coalesced row reads (a warp reads consecutive steps of one
     // node) staged through shared memory, then into the register window
-    stage_rows<L, LEAN>(s_out, a.src, a.radd, rowb, N, a.t0, mreal, len);
+    stage_rows<L, LEAN>(s_out, (PAIR && half) ? a.src2 : a.src, a.radd, rowb, N, t0, mreal, len, PAIR && half);
     __syncthreads();
     if (stamp) a.dbg_clk[15] = clock64();
     double tile[NPT][L];
@@ -369,44 +420,17 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 #pragma unroll
         for (int k = 0; k < L; ++k) tile[v][k] = (valid && k < len) ? s_out[q * (L + 1) + k] : 0.0;
     }
-    if constexpr (PC && MODE == 1) {
+    if constexpr (PC && MODE == 1 && !PAIR) {
         if (a.fuse0) {
             // level-0 history product (n = 64) of the previous leaf onto this one:
             // tile[v][k] -= sum_j col[32 + k - j] U[row][t0 - 32 + j] (lags 1..63), with the
-            // previous leaf's U staged through s_out (free until the step loop writes it).
-            // Rolled over output chunks (instruction footprint): the weights are constant-bank
-            // operands at a CTA-uniform runtime offset (kc[0 .. 2L) holds lags 0 .. 2L-1), each
-            // chunk's sums go back to the thread's own row of s_out and are subtracted from the
-            // register window afterwards.
+            // previous leaf's U staged through s_out (free until the step loop writes it);
+            // the sums go back to the thread's own rows and are subtracted from the window.
             __syncthreads();
-            stage_rows<L, LEAN>(s_out, a.X, nullptr, rowb, N, a.t0 - L, mreal, L);
+            stage_rows<L, LEAN>(s_out, a.X, nullptr, rowb, N, t0 - L, mreal, L);
             __syncthreads();
             if (stamp) a.dbg_clk[5] = clock64();
-#pragma unroll 1
-            for (int v = 0; v < NPT; ++v) {
-                const int q = tid * NPT + v;
-                if (q >= mreal) continue;
-                double* row = s_out + q * (L + 1);
-                double u[L];
-#pragma unroll
-                for (int jj = 0; jj < L; ++jj) u[jj] = row[jj];
-                // 8 outputs at a time: each output sums jj ascending (bitwise equal to the
-                // standalone direct product) with 8 independent FMA chains in flight
-#pragma unroll 1
-                for (int k0 = 0; k0 < L; k0 += 8) {
-                    const double* wp = a.kc + L + k0;  // wp[kk - jj]: weight of lag L + k0 + kk - jj
-                    double acc[8];
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.0;
-#pragma unroll
-                    for (int jj = 0; jj < L; ++jj) {
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) acc[kk] = fma(wp[kk - jj], u[jj], acc[kk]);
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) row[k0 + kk] = acc[kk];
-                }
-            }
+            level0_rows<NPT, L>(a, s_out, tid, mreal);
             // (own rows only: no barrier)
 #pragma unroll
             for (int v = 0; v < NPT; ++v) {
@@ -422,7 +446,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         // fused separable RHS (ft_solve_fast_modes): tile += sum_j A[row][j] T[pb][t][j]
         // straight into the register window; T is warp-uniform (broadcast loads)
         const int J = a.genJ;
-        const double* Tb = a.genT + ((uint64_t)pb * N + a.t0) * J;
+        const double* Tb = a.genT + ((uint64_t)pb * N + t0) * J;
         constexpr int kMaxJ = 16;
         __shared__ double s_T[kMaxJ][L];  // this leaf's step factors, [j][k] (broadcast reads)
         for (int e = tid; e < kMaxJ * L; e += blockDim.x) {
@@ -538,16 +562,16 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
     __syncthreads();
     if (stamp) a.dbg_clk[10] = clock64();
     // coalesced store of the solution tile: consecutive threads write consecutive steps of a row
-    if (write_x) store_rows<L, LEAN>(a.X, s_out, rowb, N, a.t0, mreal, len, tid, blockDim.x);
+    if (write_x) store_rows<L, LEAN>(a.X, s_out, rowb, N, t0, mreal, len, tid, blockDim.x);
     if (!LEAN && MODE == 0 && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1) (single-slab problems)
         for (int e = tid; e < mreal * len; e += blockDim.x) {
             const int q = e / len, k = e - q * len;
             const double up = q > 0 ? s_out[(q - 1) * (L + 1) + k] : 0.0;
-            a.V[(rowb + q) * N + a.t0 + k] = s_out[q * (L + 1) + k] + up;
+            a.V[(rowb + q) * N + t0 + k] = s_out[q * (L + 1) + k] + up;
         }
     }
     if (MODE == 1) {
-        double* xo = a.xsend + (uint64_t)cta * L * 2;
+        double* xo = a.xsend + (uint64_t)cta * L * 2 + (PAIR ? (uint64_t)half * gridDim.x * L * 2 : 0);
         for (int i = tid; i < 2 * len; i += blockDim.x) xo[i] = (&s_cx[0][0])[i];
     }
     if (stamp) a.dbg_clk[11] = clock64();
@@ -705,8 +729,9 @@ __global__ void __launch_bounds__(kMaxSlabs / 32 * 32 + 32) leaf_wbuild(LeafArgs
 // own slab over them, and a butterfly reduce-scatter + cross-warp sum folds
 // the 256 partial vectors (fixed order: bitwise reproducible, independent of
 // how slabs are partitioned over ranks).
-template <int KIND, int NPT, int L, bool LEAN = false>
-__device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, double* s_x, bool x_resident) {
+template <int KIND, int NPT, int L, bool LEAN = false, bool PAIR = false>
+__device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, double* s_x, bool x_resident,
+                                             int half = 0) {
     // s_c0: carries of every slab transposed to [L][2P + 1]; s_x: [m][L+1] phase-1 solution tile
     __shared__ double s_inj[L][2];          // this slab's EL_k, ER_k
     __shared__ double s_red[kLeafThreads / 32][2 * L];
@@ -723,7 +748,10 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
     if (stamp) a.dbg_clk[0] = clock64();
     // load the carries of every slab of this problem (transposed) and the phase-1 tile
-    const double* xin = a.xch + (uint64_t)pb * P * L * 2;
+    const uint64_t t0 = a.t0 + (PAIR ? (uint64_t)half * L : 0);
+    // (pair kernel: the second leaf's carries use the other half of the double-sized buffer, so
+    // a fast CTA's phase 1 never overwrites carries a slow CTA is still reading)
+    const double* xin = a.xch + (uint64_t)pb * P * L * 2 + (PAIR ? (uint64_t)half * gridDim.x * L * 2 : 0);
     {   // 16-byte loads (one step's two carries of a slab), 16 in flight per thread
         const double2* xin2 = reinterpret_cast<const double2*>(xin);
         const int total2 = P * L;
@@ -880,12 +908,12 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     }
     __syncthreads();
     if (stamp) a.dbg_clk[3] = clock64();
-    store_rows<L, LEAN>(a.X, s_x, rowb, a.N, a.t0, mreal, len, tid, blockDim.x);
+    store_rows<L, LEAN>(a.X, s_x, rowb, a.N, t0, mreal, len, tid, blockDim.x);
     if (!LEAN && a.V) {  // Scheme 2 product sources V = U_i + U_(i-1); the slab's left neighbour value is EL
         for (int e = tid; e < mreal * len; e += blockDim.x) {
             const int q = e / len, k = e - q * len;
             const double left = q > 0 ? s_x[(q - 1) * (L + 1) + k] : s_inj[k][0];
-            a.V[(rowb + q) * a.N + a.t0 + k] = s_x[q * (L + 1) + k] + left;
+            a.V[(rowb + q) * a.N + t0 + k] = s_x[q * (L + 1) + k] + left;
         }
     }
     if (stamp) a.dbg_clk[4] = clock64();
@@ -947,6 +975,49 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     __syncthreads();
     if (stamp) a.dbg_clk[13] = clock64();
     correct_body<KIND, NPT, L, LEAN>(a, s_c0, s_x, true);
+}
+
+// Two consecutive slab leaves in one cooperative kernel (single-GPU plans whose level-0
+// history products fold into the leaf: between leaves 2i and 2i+1 the schedule has no other
+// product).  The first leaf's solution stays in shared memory, so the level-0 product reads
+// it there (no re-staging of U from global memory), the second leaf's R tile is prefetched
+// into L2 while the first leaf runs, and one launch per pair disappears.  The body is a
+// rolled loop over the two leaves: the instruction footprint is that of one leaf.
+template <int KIND, int NPT, int L>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_pair(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    double* s_c0 = s_dyn;
+    double* s_x = s_dyn + (uint64_t)L * (2 * a.P + 1);
+    const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) a.dbg_clk[12] = clock64();
+    prefetch_correct_tables<L>(a);
+    {   // the second leaf's R tile (final since the last product kernel): into L2 now
+        const int cta = blockIdx.x;
+        const int pb = cta / a.P_local, s = a.s_begin + (cta - pb * a.P_local);
+        const int slab0 = s * a.slab;
+        const int mreal = min(a.slab, a.nodes - slab0);
+        const uint64_t rowb = (uint64_t)pb * a.rows_pp + (slab0 - a.node_begin);
+        for (int e = threadIdx.x; e < 2 * mreal; e += blockDim.x)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.src2 + (rowb + (e >> 1)) * a.N + a.t0 + L + (e & 1) * 16));
+    }
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        leaf_body<KIND, NPT, L, 1, true, true, true>(a, s_x, false, half);
+        __syncthreads();
+        if (stamp) a.dbg_clk[14] = clock64();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(a.bar, 1u);
+            const unsigned target = a.bar_target + (unsigned)half * gridDim.x;
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+            } while (v < target);
+        }
+        __syncthreads();
+        if (stamp) a.dbg_clk[13] = clock64();
+        correct_body<KIND, NPT, L, true, true>(a, s_c0, s_x, true, half);
+    }
 }
 
 // Partitioned slab leaf with the carry exchange done by the kernel itself over
@@ -1068,6 +1139,28 @@ static cudaError_t launch_fused_t(const LeafArgs& a, int ctas, cudaStream_t st) 
 }
 
 template <int KIND, int NPT, int L>
+static cudaError_t launch_pair_t(const LeafArgs& a, int ctas, cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
+    static DeviceOnce attr;
+    if (attr.first()) {
+        cudaFuncSetAttribute(leaf_pair<KIND, NPT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * (L * (2 * kMaxSlabs + 1) + kLeafThreads * NPT * (L + 1))));
+        attr.done();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLeafThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute coop[1];
+    coop[0].id = cudaLaunchAttributeCooperative;
+    coop[0].val.cooperative = 1;
+    cfg.attrs = coop;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, leaf_pair<KIND, NPT, L>, a);
+}
+
+template <int KIND, int NPT, int L>
 static cudaError_t launch_p2p_t(const LeafArgs& a, int ctas, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)L * (2 * a.P + 1) + (size_t)kLeafThreads * NPT * (L + 1));
     static DeviceOnce attr;
@@ -1095,6 +1188,20 @@ cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int cta
     if (npt == 2 && L == 32) {
         if (kind == SK_TRIDIAG) return launch_p2p_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
         if (kind == SK_UPWIND) return launch_p2p_t<SK_UPWIND, 2, 32>(a, ctas, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// both leaves whole, even N, R from arrays, single-problem constants: see leaf_pair
+bool leaf_pair_ok(const LeafArgs& a, int L) {
+    static const bool off = getenv("FT_NO_PAIR") != nullptr;
+    return !off && a.kc_valid && a.len == L && (a.N & 1) == 0 && !a.radd && !a.genA && !a.V && !a.stencil;
+}
+
+cudaError_t launch_leaf_pair(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
+    if (npt == 2 && L == 32) {
+        if (kind == SK_TRIDIAG) return launch_pair_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
+        if (kind == SK_UPWIND) return launch_pair_t<SK_UPWIND, 2, 32>(a, ctas, st);
     }
     return cudaErrorInvalidValue;
 }
