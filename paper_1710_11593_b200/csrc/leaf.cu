@@ -1194,7 +1194,7 @@ cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int cta
 
 // both leaves whole, even N, R from arrays, single-problem constants: see leaf_pair
 bool leaf_pair_ok(const LeafArgs& a, int L) {
-    static const bool off = getenv("FT_NO_PAIR") != nullptr;
+    static const bool off = getenv("FT_NO_PAIR") != nullptr || getenv("FT_NO_LEAN") != nullptr;
     return !off && a.kc_valid && a.len == L && (a.N & 1) == 0 && !a.radd && !a.genA && !a.V && !a.stencil;
 }
 

@@ -947,6 +947,209 @@ __global__ void __launch_bounds__(kMpThreads, FT_MP1G_MINB) mp1g_kernel(MpArgs a
     }
 }
 
+// ---- persistent, TMA-staged variant of mp1g_kernel ------------------------------
+// One CTA per SM slot loops over tiles of G = kMpTile / n row pairs.  While a tile is being
+// transformed, the NEXT tile's source rows (G pairs x 2 rows x h doubles = 32 KB, one
+// contiguous segment per row) are copied HBM -> shared memory by the TMA unit
+// (cp.async.bulk, completion counted on an mbarrier) and the lines of its targets are
+// prefetched into L2; pass 0 then reads its inputs from shared memory.  ncu on mp1g_kernel:
+// the first use of the source loads was 10 % of all stall samples (HBM latency exposed once
+// per CTA, two CTAs per SM).  Needs 16-byte aligned row segments (even N; lo is a multiple
+// of the leaf length).  Measured on B200 (round 2): correct, but slower than mp1g_kernel
+// (see launch_mp1), so it is opt-in (FT_MP1P=1) and kept as the TMA reference point.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(kMpThreads, 2) mp1p_kernel(MpArgs a, int ntiles) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
+    using PL = Plan1<LOGN>;
+    constexpr int n = PL::n, h = PL::h, Q0 = PL::Q0, RL = PL::RL;
+    static_assert(n <= kMpTile, "group-private plan needs n <= kMpTile");
+    constexpr int G = kMpTile / n, GT = n / 16;
+    constexpr int total = kMpTile;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    double* stage = reinterpret_cast<double*>(buf + spad_len(total));  // [G][2][h] source rows of the tile
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(stage + 2 * G * h);
+    const int tid = threadIdx.x;
+    const int g = tid / GT, j = tid - g * GT;
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const uint64_t N = a.N;
+    const uint64_t tend = a.hi < N ? a.hi : N;
+
+    // issue (tid < 2G): row (tid & 1) of pair tid >> 1 of tile t -> stage; every issuer arrives
+    auto issue = [&](int t) {
+        if (tid < 2 * G) {
+            const int pg = tid >> 1, r = tid & 1;
+            const int pair = t * G + pg;
+            const int pb = min(pair, npairs - 1) / a.pairs_per_problem;
+            const int lp = min(pair, npairs - 1) - pb * a.pairs_per_problem;
+            const bool ok = pair < npairs && 2 * lp + r < a.nodes;
+            if (ok) {
+                mbar_arrive_expect_tx(mbar, h * 8);
+                bulk_g2s(stage + (size_t)(2 * pg + r) * h, a.U + ((uint64_t)(pb * a.nodes + 2 * lp + r)) * N + a.lo,
+                         h * 8, mbar);
+            } else {
+                mbar_arrive_expect_tx(mbar, 0);
+            }
+        }
+        // the tile's targets: into L2 while the previous tile is transformed (128-byte lines)
+        if (a.rsrc) {
+            constexpr int LPR = h * 8 / 128 > 0 ? h * 8 / 128 : 1;  // lines per row
+            for (int e = tid; e < 2 * G * LPR; e += kMpThreads) {
+                const int rr = e / LPR, ln = e - rr * LPR;
+                const int pair = t * G + (rr >> 1);
+                const int pb = min(pair, npairs - 1) / a.pairs_per_problem;
+                const int lp = min(pair, npairs - 1) - pb * a.pairs_per_problem;
+                if (pair < npairs && 2 * lp + (rr & 1) < a.nodes && a.mid + (uint64_t)ln * 16 < tend)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rsrc + ((uint64_t)(pb * a.nodes + 2 * lp + (rr & 1))) * N +
+                                                                     a.mid + (uint64_t)ln * 16));
+            }
+        }
+    };
+    if (tid == 0) {
+        mbar_init(mbar, 2 * G);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int tile = blockIdx.x;
+    if (tile < ntiles) issue(tile);
+    unsigned parity = 0;
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int pair = tile * G + g;
+        const bool live = pair < npairs;
+        PairInfo pi;
+        {
+            const int rp = min(pair, npairs - 1);
+            const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+            pi = {(uint64_t)(pb * a.nodes + 2 * lp), pb, (live && 2 * lp + 1 < a.nodes) ? 1 : 0};
+        }
+        // pass 0 (S = n, radix 16) from the staged rows; inputs p >= 8 are the zero padding
+        {
+            cplx w[16];
+            pass_twiddles<16>(w, a.tw, n, j);
+            mbar_wait(mbar, parity);
+            parity ^= 1u;
+            const double* s1 = stage + (size_t)(2 * g) * h + j;
+            cplx v[16];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                v[p].x = live ? s1[p * Q0] : 0.0;
+                v[p].y = (live && pi.has2) ? s1[h + p * Q0] : 0.0;
+            }
+            __syncthreads();  // every thread has its inputs (and is done with the previous tile)
+            if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x);
+            dft_reg_halfzero<16>(v);
+#pragma unroll
+            for (int q = 1; q < 16; ++q) v[q] = cmul(v[q], w[q]);
+            const int pb = sphys(g * n + j);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) buf[pb + q * (Q0 + (Q0 >> 4))] = v[q];
+        }
+        mid_fwd_g<LOGN - 4, LOGN>(buf, total, a.tw, g);
+
+        // fused pass: this group's tasks t = g*(n/RL) + j + k*GT, k < 16/RL
+        constexpr int FT = 16 / RL;
+        {
+            cplx spv[16];
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+                const int base = (g * (n / RL) + j + k * GT) * RL;
+                const cplx* sp = a.spec + (uint64_t)pi.pb * n + (base & (n - 1));
+#pragma unroll
+                for (int p = 0; p < RL; ++p) spv[k * RL + p] = ldgc(&sp[p]);
+            }
+            GroupSync<LOGN>::sync(g);
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+                const int pbx = sphys((g * (n / RL) + j + k * GT) * RL);
+                cplx v[RL];
+#pragma unroll
+                for (int p = 0; p < RL; ++p) v[p] = buf[pbx + p];
+                dft_reg<RL, false>(v);
+#pragma unroll
+                for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], spv[k * RL + p]);
+                dft_reg<RL, true>(v);
+#pragma unroll
+                for (int p = 0; p < RL; ++p) buf[pbx + p] = v[p];
+            }
+        }
+        mid_inv_g<LOGN - 4, LOGN>(buf, total, a.tw, g);
+
+        // last inverse pass (S = n, radix 16): outputs p >= 8 are the targets [mid, mid + h)
+        double r1[8], r2[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
+            const bool ok = live && tt < tend;
+            r1[p] = (ok && a.rsrc) ? a.rsrc[pi.row1 * N + tt] : 0.0;
+            r2[p] = (ok && pi.has2 && a.rsrc) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
+        }
+        cplx w[16];
+        pass_twiddles<16>(w, a.tw, n, j);
+        GroupSync<LOGN>::sync(g);
+        const int pbx = sphys(g * n + j);
+        cplx v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = buf[pbx + q * (Q0 + (Q0 >> 4))];
+#pragma unroll
+        for (int q = 1; q < 16; ++q) v[q] = cmulc(v[q], w[q]);
+        dft_reg<16, true>(v);
+        if (live) {
+#pragma unroll
+            for (int p = 8; p < 16; ++p) {
+                const uint64_t tt = a.mid + j + (uint64_t)(p - 8) * Q0;
+                if (tt >= tend) continue;
+                cplx y = v[p];
+                const int tp = (int)(tt - a.mid);
+                if (tp < a.J - 1) {  // exact near field: lags t - j < J
+                    const double* cp = a.col + (uint64_t)pi.pb * N;
+                    const double* xr = a.U + pi.row1 * N;
+                    const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
+                    double s1 = 0.0, s2 = 0.0;
+                    for (uint64_t jj = a.mid; jj-- > jlo;) {
+                        const double cv = cp[tt - jj];
+                        s1 = fma(cv, xr[jj], s1);
+                        if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
+                    }
+                    y.x += s1;
+                    y.y += s2;
+                }
+                a.X[pi.row1 * N + tt] = r1[p - 8] - y.x;
+                if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 8] - y.y;
+            }
+        }
+        // (the next tile's pass 0 writes this group's region of buf only after the CTA barrier
+        // that every thread reaches after finishing the reads above)
+    }
+}
+
 // Spectrum of one level for the single-CTA plan: full n-point column (lags
 // J <= k < min(n, N)), same passes, scaled 1/n, stored in plan order.
 template <int LOGN>
@@ -1291,6 +1494,28 @@ static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
             if (gattr.first()) {
                 cudaFuncSetAttribute(mp1g_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 gattr.done();
+            }
+            // persistent TMA-staged variant (opt-in, FT_MP1P=1: measured slower than the plain
+            // launch -- cfg4 388 vs 366 ms, n = 4096 level 3.65 vs 2.89 ms per launch: the CTA
+            // barrier per tile re-synchronises the groups and the hardware CTA scheduler already
+            // overlaps one CTA's loads with the other's transform); 16-byte aligned row segments
+            static const bool tma = getenv("FT_MP1P") != nullptr;
+            if (tma && (a.N & 1) == 0 && (a.lo & 1) == 0 && a.mid - a.lo == (uint64_t)(n / 2)) {
+                static DeviceOnce pattr;
+                const size_t psmem = smem + sizeof(double) * 2 * G * (n / 2) + 16;
+                static int slots = 0;
+                if (pattr.first()) {
+                    cudaFuncSetAttribute(mp1p_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+                    pattr.done();
+                }
+                if (slots == 0) {
+                    int dev = 0, sms = 0, per = 0;
+                    cudaGetDevice(&dev);
+                    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mp1p_kernel<LOGN>, kMpThreads, psmem);
+                    slots = sms * (per > 0 ? per : 1);
+                }
+                return launch_ex(mp1p_kernel<LOGN>, dim3(std::min(ctas, slots)), dim3(kMpThreads), psmem, st, 1, a, ctas);
             }
             return launch_ex(mp1g_kernel<LOGN>, dim3(ctas), dim3(kMpThreads), smem, st, 1, a);
         }
