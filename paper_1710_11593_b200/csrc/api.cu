@@ -152,7 +152,8 @@ uint64_t rows_of(const ft_plan* p) { return (uint64_t)p->B * (uint64_t)p->local_
 // 100 vs 102 ms); device-buffer solves without fused RHS generation.
 bool fuse0_plan(const ft_plan* p) {
     static const bool off = getenv("FT_NO_FUSE0") != nullptr;
-    return !off && p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= 8 &&
+    static const int min_p = getenv("FT_FUSE0_MIN_P") ? atoi(getenv("FT_FUSE0_MIN_P")) : 8;
+    return !off && p->multi && p->part_world == 1 && p->fused_leaf && p->L == 32 && p->B == 1 && p->P >= min_p &&
            !p->stencil;
 }
 
