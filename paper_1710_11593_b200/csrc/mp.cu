@@ -947,6 +947,257 @@ __global__ void __launch_bounds__(kMpThreads, FT_MP1G_MINB) mp1g_kernel(MpArgs a
     }
 }
 
+// ---- radix-8, high-occupancy variant (256 <= n <= 4096; opt-in, FT_MP8=0x1f00) -----------
+// mp1g_kernel holds 16 complex points per thread (128 registers): 16 warps per SM, and ncu
+// shows the FP64 pipe ~50 % busy with every warp waiting on fixed-latency, shared-memory and
+// global-load dependencies.  This variant tests the occupancy hypothesis: 8 points per thread
+// in radix-8 passes at <= 85 registers, 24 warps per SM (3 CTAs of 256 threads and a
+// 2048-point tile for n <= 2048; FT_MP8_MINB=4: <= 64 registers with ~400 B of spills, 32
+// warps).  Same structure otherwise: pass 0 from HBM with the zero half pruned, group-private
+// barriers, last forward pass + spectrum + first inverse pass fused in registers, last
+// inverse pass straight to HBM.  Shared-memory padding is one slot per 8 points
+// (conflict-free 16-byte accesses for every pass stride and for the 8 contiguous points of
+// the fused pass).  The spectrum comes from spec8_kernel (same pass plan, so the
+// digit-reversed orders agree).
+// Measured on B200 (round 2, cfg4 per level, ms; mp1g / mp8 at 24 warps / mp8 at 32 warps):
+//   n = 256: 20.1 / 21.6 / 27.2   512: 18.4 / 22.9 / 28.9   1024: 20.5 / 27.1 / 34.7
+//   2048: 24.5 / 28.0 / 36.6      4096: 23.0 / 31.2 / 44.6
+// More warps do not help: the level is bound by the shared-memory / L1 data path and the
+// FP64 pipe together (each ~50-55 % busy in mp1g), and radix 8 adds shared-memory round
+// trips and twiddle loads per point.  Kept as the measured reference point, not the default.
+__device__ __forceinline__ int sphys8(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int sphys8_len(int n) { return n + (n >> 3) + 1; }
+#ifndef FT_MP8_DEFAULT
+#define FT_MP8_DEFAULT 0
+#endif
+
+template <int LOGN>
+struct Plan8 {
+    static constexpr int n = 1 << LOGN;
+    static constexpr int NP = (LOGN - 1) / 3;      // radix-8 passes before the fused one
+    static constexpr int LOGRL = LOGN - 3 * NP;    // fused radix 2, 4 or 8
+    static constexpr int RL = 1 << LOGRL;
+    static constexpr int Q0 = n / 8;
+    static constexpr int GT = n / 8;               // threads per pair
+    static constexpr int TPB = GT < 256 ? 256 : GT;
+    static constexpr int TILE = TPB * 8;
+    static constexpr int G = TILE / n;
+};
+
+template <int GT, int TPB>
+__device__ __forceinline__ void group_sync8(int g) {
+    if constexpr (GT <= 32) {
+        __syncwarp();
+    } else if constexpr (GT < TPB) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GT) : "memory");
+    } else {
+        __syncthreads();
+    }
+}
+
+// one radix-8 pass of group size S = 2^LOGS over this thread's butterfly (tl = thread within the pair)
+template <int LOGS, bool INV>
+__device__ __forceinline__ void pass8(cplx* gb, int tl, const cplx* __restrict__ tw) {
+    constexpr int LOGQ = LOGS - 3, Q = 1 << LOGQ, S = 1 << LOGS;
+    const int j = tl & (Q - 1);
+    const int base = ((tl >> LOGQ) << LOGS) + j;
+    cplx* b = gb + sphys8(base);
+    cplx v[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) v[p] = b[p * Q + ((p * Q) >> 3)];
+    if (!INV) {
+        dft_reg<8, false>(v);
+        cplx w[8];
+        pass_twiddles<8>(w, tw, S, j);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) v[q] = cmul(v[q], w[q]);
+    } else {
+        cplx w[8];
+        pass_twiddles<8>(w, tw, S, j);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) v[q] = cmulc(v[q], w[q]);
+        dft_reg<8, true>(v);
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) b[p * Q + ((p * Q) >> 3)] = v[p];
+}
+
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_fwd8(cplx* gb, int tl, const cplx* tw, int g) {
+    using PL = Plan8<LOGN>;
+    if constexpr (LOGS > PL::LOGRL) {
+        group_sync8<PL::GT, PL::TPB>(g);
+        pass8<LOGS, false>(gb, tl, tw);
+        mid_fwd8<LOGS - 3, LOGN>(gb, tl, tw, g);
+    }
+}
+template <int LOGS, int LOGN>
+__device__ __forceinline__ void mid_inv8(cplx* gb, int tl, const cplx* tw, int g) {
+    using PL = Plan8<LOGN>;
+    if constexpr (LOGS > PL::LOGRL) {
+        mid_inv8<LOGS - 3, LOGN>(gb, tl, tw, g);
+        group_sync8<PL::GT, PL::TPB>(g);
+        pass8<LOGS, true>(gb, tl, tw);
+    }
+}
+
+template <int LOGN>
+#ifndef FT_MP8_MINB
+#define FT_MP8_MINB 3  // CTAs of 256 threads per SM (3: <= 85 registers, no spills; 4: <= 64)
+#endif
+__global__ void __launch_bounds__(Plan8<LOGN>::TPB, FT_MP8_MINB * 256 / Plan8<LOGN>::TPB) mp8_kernel(MpArgs a) {
+    pdl_launch_dependents(a.pdl_trigger);
+    pdl_wait();
+    using PL = Plan8<LOGN>;
+    constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL, GT = PL::GT, G = PL::G;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int g = tid / GT, j = tid - g * GT;
+    cplx* gb = buf + sphys8(g * n);
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    const int pair = blockIdx.x * G + g;
+    const bool live = pair < npairs;
+    const uint64_t N = a.N;
+    PairInfo pi;
+    {
+        const int rp = min(pair, npairs - 1);
+        const int pb = rp / a.pairs_per_problem, lp = rp - pb * a.pairs_per_problem;
+        pi = {(uint64_t)(pb * a.nodes + 2 * lp), pb, (live && 2 * lp + 1 < a.nodes) ? 1 : 0};
+    }
+    // pass 0 (S = n) from HBM; inputs p >= 4 are the zero padding
+    {
+        const double* x1 = a.U + pi.row1 * N + a.lo + j;
+        cplx v[8];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            v[p].x = live ? x1[(uint64_t)p * Q0] : 0.0;
+            v[p].y = (live && pi.has2) ? x1[N + (uint64_t)p * Q0] : 0.0;
+        }
+        dft_reg_halfzero<8>(v);
+        cplx w[8];
+        pass_twiddles<8>(w, a.tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) v[q] = cmul(v[q], w[q]);
+        cplx* b = gb + sphys8(j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) b[q * (Q0 + (Q0 >> 3))] = v[q];
+    }
+    mid_fwd8<LOGN - 3, LOGN>(gb, j, a.tw, g);
+    // fused: last forward pass (radix RL, twiddle-free), spectrum, first inverse pass, on the
+    // 8 contiguous points 8 j .. 8 j + 7 of the pair
+    {
+        const cplx* sp = a.spec + (uint64_t)pi.pb * n + 8 * j;
+        cplx spv[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) spv[p] = ldgc(&sp[p]);
+        group_sync8<GT, PL::TPB>(g);
+        cplx* b = gb + 9 * j;  // sphys8(8 j)
+#pragma unroll
+        for (int k = 0; k < 8 / RL; ++k) {
+            cplx v[RL];
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = b[k * RL + p];
+            dft_reg<RL, false>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) v[p] = cmul(v[p], spv[k * RL + p]);
+            dft_reg<RL, true>(v);
+#pragma unroll
+            for (int p = 0; p < RL; ++p) b[k * RL + p] = v[p];
+        }
+    }
+    mid_inv8<LOGN - 3, LOGN>(gb, j, a.tw, g);
+    // last inverse pass (S = n): outputs p >= 4 are the targets [mid, mid + h)
+    const uint64_t tend = a.hi < N ? a.hi : N;
+    cplx w[8];
+    pass_twiddles<8>(w, a.tw, n, j);
+    group_sync8<GT, PL::TPB>(g);
+    cplx v[8];
+    {
+        const cplx* b = gb + sphys8(j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = b[q * (Q0 + (Q0 >> 3))];
+    }
+#pragma unroll
+    for (int q = 1; q < 8; ++q) v[q] = cmulc(v[q], w[q]);
+    double r1[4], r2[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)p * Q0;
+        const bool ok = live && tt < tend;
+        r1[p] = (ok && a.rsrc) ? a.rsrc[pi.row1 * N + tt] : 0.0;
+        r2[p] = (ok && pi.has2 && a.rsrc) ? a.rsrc[(pi.row1 + 1) * N + tt] : 0.0;
+    }
+    dft_reg<8, true>(v);
+    if (!live) return;
+#pragma unroll
+    for (int p = 4; p < 8; ++p) {
+        const uint64_t tt = a.mid + j + (uint64_t)(p - 4) * Q0;
+        if (tt >= tend) continue;
+        cplx y = v[p];
+        const int tp = (int)(tt - a.mid);
+        if (tp < a.J - 1) {  // exact near field: lags t - j < J
+            const double* cp = a.col + (uint64_t)pi.pb * N;
+            const double* xr = a.U + pi.row1 * N;
+            const uint64_t jlo = (tt >= a.lo + (uint64_t)(a.J - 1)) ? tt - (uint64_t)(a.J - 1) : a.lo;
+            double s1 = 0.0, s2 = 0.0;
+#pragma unroll 1
+            for (uint64_t jj = a.mid; jj-- > jlo;) {
+                const double cv = cp[tt - jj];
+                s1 = fma(cv, xr[jj], s1);
+                if (pi.has2) s2 = fma(cv, xr[N + jj], s2);
+            }
+            y.x += s1;
+            y.y += s2;
+        }
+        a.X[pi.row1 * N + tt] = r1[p - 4] - y.x;
+        if (pi.has2) a.X[(pi.row1 + 1) * N + tt] = r2[p - 4] - y.y;
+    }
+}
+
+// Spectrum of one level in the radix-8 plan order: full n-point column (lags J <= k < min(n, N)),
+// scaled 1/n.  One CTA of n / 8 threads per problem.
+template <int LOGN>
+__global__ void __launch_bounds__(Plan8<LOGN>::GT, 1) spec8_kernel(const double* col, uint64_t N, int J, cplx* spec,
+                                                                   const cplx* tw) {
+    using PL = Plan8<LOGN>;
+    constexpr int n = PL::n, Q0 = PL::Q0, RL = PL::RL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* buf = reinterpret_cast<cplx*>(smem_raw);
+    const int pb = blockIdx.x, j = threadIdx.x;
+    const double* c = col + (uint64_t)pb * N;
+    const uint64_t kend = (uint64_t)n < N ? (uint64_t)n : N;
+    {
+        cplx v[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const uint64_t k = (uint64_t)j + (uint64_t)p * Q0;
+            v[p] = {(k >= (uint64_t)J && k < kend) ? c[k] : 0.0, 0.0};
+        }
+        dft_reg<8, false>(v);
+        cplx w[8];
+        pass_twiddles<8>(w, tw, n, j);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) v[q] = cmul(v[q], w[q]);
+        cplx* b = buf + sphys8(j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) b[q * (Q0 + (Q0 >> 3))] = v[q];
+    }
+    mid_fwd8<LOGN - 3, LOGN>(buf, j, tw, 0);
+    __syncthreads();
+    const double scale = 1.0 / (double)n;
+    cplx* b = buf + 9 * j;
+#pragma unroll
+    for (int k = 0; k < 8 / RL; ++k) {
+        cplx v[RL];
+#pragma unroll
+        for (int p = 0; p < RL; ++p) v[p] = b[k * RL + p];
+        dft_reg<RL, false>(v);
+#pragma unroll
+        for (int p = 0; p < RL; ++p) spec[(uint64_t)pb * n + 8 * j + k * RL + p] = {v[p].x * scale, v[p].y * scale};
+    }
+}
+
 // ---- persistent, TMA-staged variant of mp1g_kernel ------------------------------
 // One CTA per SM slot loops over tiles of G = kMpTile / n row pairs.  While a tile is being
 // transformed, the NEXT tile's source rows (G pairs x 2 rows x h doubles = 32 KB, one
@@ -1472,9 +1723,33 @@ bool mp_is_single(int n) {
     return !mp_is_direct(n) && n >= 256 && n <= single_max;
 }
 
+// Levels that run the radix-8 high-occupancy kernel (mp8_kernel) instead of mp1g_kernel:
+// FT_MP8 = bit mask over log2 n (bit 8 = n 256 ... bit 12 = n 4096); read once.
+bool mp8_level(int n) {
+    static const int mask = getenv("FT_MP8") ? (int)strtol(getenv("FT_MP8"), nullptr, 0) : FT_MP8_DEFAULT;
+    const int lg = __builtin_ctz(n);
+    return lg >= 8 && lg <= 12 && ((mask >> lg) & 1);
+}
+
+template <int LOGN>
+static cudaError_t launch_mp8(const MpArgs& a, cudaStream_t st) {
+    using PL = Plan8<LOGN>;
+    const size_t smem = sizeof(cplx) * (size_t)(sphys8_len(PL::TILE));
+    static DeviceOnce attr_set;
+    if (attr_set.first()) {
+        cudaFuncSetAttribute(mp8_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set.done();
+    }
+    const int npairs = (a.rows / a.nodes) * a.pairs_per_problem;
+    return launch_ex(mp8_kernel<LOGN>, dim3((npairs + PL::G - 1) / PL::G), dim3(PL::TPB), smem, st, 1, a);
+}
+
 template <int LOGN>
 static cudaError_t launch_mp1(const MpArgs& a, cudaStream_t st) {
     constexpr int n = 1 << LOGN;
+    if constexpr (LOGN <= 12) {
+        if (mp8_level(n)) return launch_mp8<LOGN>(a, st);
+    }
     constexpr int G = n >= kMpTile ? 1 : kMpTile / n;  // as in mp1_kernel
 #ifndef FT_MP1_SMEM_PAD
 #define FT_MP1_SMEM_PAD 0
@@ -1527,6 +1802,19 @@ template <int LOGN>
 static cudaError_t launch_spec1(const double* col, uint64_t N, int B, int J, cplx* spec, const cplx* tw,
                                 cudaStream_t st) {
     constexpr int n = 1 << LOGN;
+    if constexpr (LOGN <= 12) {
+        if (mp8_level(n)) {
+            using PL = Plan8<LOGN>;
+            const size_t smem8 = sizeof(cplx) * (size_t)(sphys8_len(n));
+            static DeviceOnce attr8;
+            if (attr8.first()) {
+                cudaFuncSetAttribute(spec8_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
+                attr8.done();
+            }
+            spec8_kernel<LOGN><<<B, PL::GT, smem8, st>>>(col, N, J, spec, tw);
+            return cudaGetLastError();
+        }
+    }
     static DeviceOnce attr_set;
     if (attr_set.first()) {
         cudaFuncSetAttribute(spec1_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -313,6 +313,32 @@ def test_fused_rhs_generation(ft, oracle_mod, cid, kw, rhs_mode):
     assert np.array_equal(Uh, Ug.cpu().numpy())
 
 
+@pytest.mark.parametrize("cid,kw,rhs_mode", [
+    (1, dict(time_steps=1000), 0),
+    (2, dict(time_steps=700, cells=33), 0),
+    (3, dict(time_steps=512, cells=17), 0),
+    (4, dict(time_steps=256, cells=3001), 0),     # cooperative slab leaf, folded level-0 products
+    (5, dict(time_steps=1024, batch=3), 0),
+], ids=["cfg1", "cfg2", "cfg3", "cfg4-multislab", "cfg5"])
+def test_fused_rhs_against_cpu_oracle(ft, oracle_mod, cid, kw, rhs_mode, record_property):
+    """ft_solve_fast_modes against the CPU oracle directly (not against another CUDA path):
+    the oracle evaluates the same separable forcing with glibc's libm on the grid
+    (forcing_grid: the callback the reference's solve(spec) would be given,
+    schemes.cpp:401-408) and marches in the reference's order."""
+    import torch
+
+    w = W.config(cid, **kw)
+    F, u0, phi = _inputs(oracle_mod, w)
+    ref = oracle_mod.direct(w, F, u0, phi, rhs_mode=rhs_mode)
+    plan = ft.Plan(w.specs, rhs_mode=rhs_mode)
+    Ug = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    _, rep = plan.solve_fast_modes(Ug, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    err = oracle_mod.relerr(Ug.cpu().numpy(), ref)
+    record_property("fused_vs_cpu_oracle", err)
+    assert rep.kernel_launches > 0
+    assert err <= TOL, f"rel err {err:.3e}"
+
+
 def test_fused_rhs_streamed_to_pinned_host(ft):
     """ft_solve_fast_modes into pinned host memory streams U back chunk by chunk
     while the solve runs: bitwise equal to the device-buffer call (same kernels,

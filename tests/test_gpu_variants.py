@@ -11,6 +11,7 @@ oracle by tests/test_gpu_scale.py).  Tolerance (north_star): 1e-10 relative.
   FT_NO_PAIR=1   one cooperative kernel per leaf (leaf_fused, level-0 product from global memory)
   FT_NO_LEAN=1   the generic slab-leaf instantiation (and no pairs)
   FT_MP1P=1      persistent TMA-staged FFT levels (mp1p_kernel: cp.async.bulk + mbarrier)
+  FT_MP8=0x1f00  radix-8 high-occupancy FFT levels (mp8_kernel, n = 256 .. 4096) and their spectra
 """
 import os
 import subprocess
@@ -45,7 +46,7 @@ sys.exit(0 if worst <= 1e-10 else 1)
 
 def _run(env_extra):
     env = dict(os.environ)
-    for k in ("FT_NO_PAIR", "FT_NO_LEAN", "FT_MP1P"):
+    for k in ("FT_NO_PAIR", "FT_NO_LEAN", "FT_MP1P", "FT_MP8"):
         env.pop(k, None)
     env.update(env_extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
@@ -76,3 +77,7 @@ def test_generic_slab_leaf_variant():
 
 def test_tma_staged_fft_levels_variant():
     _run({"FT_MP1P": "1"})
+
+
+def test_radix8_high_occupancy_fft_levels_variant():
+    _run({"FT_MP8": "0x1f00"})
