@@ -210,6 +210,21 @@ int ft_solve_fast_modes(ft_plan* plan, int nmodes, const double* a, const double
                         ft_report* report);
 int ft_solve_direct(ft_plan* plan, const double* rhs, double* u, ft_report* report);
 
+/* y = A x, A the plan's block lower-triangular Toeplitz system matrix -- the operator the
+ * reference's fast path hands to GMRES (make_block_operator / make_toeplitz_operator,
+ * src/toeplitz.cpp:194-201, applied by block_matvec :150-167 through the FFT circulant
+ * embedding :84-115) and the matrix ft_solve_fast inverts.  The far history runs through the
+ * plan's own FFT / direct history products (O(M N log N), the level spectra cached at setup);
+ * the in-leaf lags and the spatial stencil are added in the difference form
+ * (d - 2b) x_i - b ((x_(i-1) - x_i) + (x_(i+1) - x_i)).  x, y: distinct device buffers,
+ * [rows][N].  Scheme 2 and partitioned plans: FT_EINVAL. */
+int ft_apply(ft_plan* plan, const double* x_device, double* y_device);
+/* max |A u - rhs| and max |rhs| over all unknowns (the reference's SolveReport::residual is
+ * GMRES's; the D&C is direct, so ft_solve_fast reports 0 and this call measures it).  work:
+ * a device buffer [rows][N] for A u, or NULL to use the plan's own work buffer. */
+int ft_residual(ft_plan* plan, const double* rhs_device, const double* u_device, double* work_device,
+                double* max_abs_residual, double* max_abs_rhs);
+
 /* Diagnostics: one fast solve (device buffers only) with a CUDA event
  * between every launch; per-launch device times for roofline accounting.
  * kind 0 = leaf, 1 = history product (level = D&C level, n = 2L << level);

@@ -101,7 +101,7 @@ ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exc
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
                "ft_solve_fast_modes", "ft_p2p_handle", "ft_p2p_connect",
                "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy",
-               "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec")
+               "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec", "ft_apply", "ft_residual")
 
 
 def lib() -> C.CDLL:
@@ -127,6 +127,8 @@ def lib() -> C.CDLL:
         L.ft_solve_fast.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_direct.argtypes = [P, P, P, C.POINTER(_Report)]
         L.ft_solve_fast_modes.argtypes = [P, I, P, P, P, P, P, P, P, C.POINTER(_Report)]
+        L.ft_apply.argtypes = [P, P, P]
+        L.ft_residual.argtypes = [P, P, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ft_p2p_handle.argtypes = [P, P]
         L.ft_p2p_connect.argtypes = [P, P]
         L.ft_set_stream.argtypes = [P, P]
@@ -373,6 +375,25 @@ class Plan:
         _check(lib().ft_profile_fast(self._h, _ptr(rhs), _ptr(out), arr, cap, C.byref(cnt)))
         return [dict(kind=arr[i].kind, level=arr[i].level, t0=arr[i].t0, len=arr[i].len,
                      bytes=arr[i].bytes, ms=arr[i].ms) for i in range(min(cnt.value, cap))]
+
+    def apply(self, x, out=None):
+        """y = A x with the plan's system matrix (device tensors; the reference's block
+        operator, applied through the plan's FFT history products)."""
+        if out is None:
+            out = x.new_empty(self.shape)
+        n = self.shape[0] * self.shape[1]
+        self._check_device(x, "x")
+        self._check_device(out, "y")
+        _check(lib().ft_apply(self._h, _ptr(x, n, "x"), _ptr(out, n, "y")))
+        return out
+
+    def residual(self, rhs, u, work=None):
+        """(max |A u - rhs|, max |rhs|) on the device."""
+        n = self.shape[0] * self.shape[1]
+        r, m = C.c_double(0.0), C.c_double(0.0)
+        _check(lib().ft_residual(self._h, _ptr(rhs, n, "rhs"), _ptr(u, n, "u"),
+                                 None if work is None else _ptr(work, n, "work"), C.byref(r), C.byref(m)))
+        return r.value, m.value
 
     def solve_fast(self, rhs, out=None):
         return self._solve(lib().ft_solve_fast, rhs, out)

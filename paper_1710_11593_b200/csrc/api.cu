@@ -1597,6 +1597,85 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
     return FT_OK;
 }
 
+// y = A x with A the plan's block lower-triangular Toeplitz system matrix (the matrix
+// ft_solve_fast inverts): far history through the schedule's own FFT / direct products
+// (O(M N log N)), in-leaf lags and the spatial stencil by apply_near_kernel.
+static int apply_impl(ft_plan* p, const double* x, double* y) {
+    if (!p || !x || !y) return set_err(FT_EINVAL, "ft_apply: bad argument");
+    if (p->stencil) return set_err(FT_EINVAL, "ft_apply: Scheme 2 (stencil history) plans are not supported");
+    if (p->part_world != 1) return set_err(FT_EINVAL, "ft_apply: partitioned plans are not supported");
+    if (!is_device_ptr(x) || !is_device_ptr(y) || x == y)
+        return set_err(FT_EINVAL, "ft_apply: x and y must be distinct device buffers");
+    FT_CUDA(cudaSetDevice(p->device));
+    cudaStream_t st = p->stream;
+    const uint64_t N = p->N;
+    FT_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * rows_of(p) * N, st));
+    for (const Op& op : p->ops) {
+        if (op.kind == OP_LEAF) continue;
+        const Level& lv = p->levels[op.level];
+        MpArgs a;
+        a.X = y;
+        a.U = x;
+        a.rsrc = y;
+        a.pdl_trigger = 0;
+        a.N = N;
+        a.lo = op.t0;
+        a.mid = op.mid;
+        a.hi = op.hi;
+        a.n = lv.n;
+        a.m = lv.m;
+        a.K = lv.K;
+        a.G = lv.G;
+        a.rows = (int)rows_of(p);
+        a.nodes = p->local_nodes;
+        a.pairs_per_problem = (p->local_nodes + 1) / 2;
+        a.spec = p->spec_d + lv.spec_off;
+        a.tw = p->tw_d;
+        a.logT = p->logT;
+        a.col = p->col_d;
+        a.J = p->J;
+        a.scratch = (lv.K >= p->split_min_k && p->split_k) ? p->mpscratch_d : nullptr;
+        a.pair_begin = 0;
+        a.pair_count = 0;
+        FT_CUDA(launch_mp(a, lv.groups, st));
+    }
+    FT_CUDA(launch_apply_near(x, y, N, p->local_nodes, rows_of(p), p->pc_d, p->col_d, p->kind, p->L, st));
+    return FT_OK;
+}
+
+int ft_apply(ft_plan* p, const double* x, double* y) {
+    const int rc = apply_impl(p, x, y);
+    if (rc) return rc;
+    FT_CUDA(cudaStreamSynchronize(p->stream));
+    return FT_OK;
+}
+
+int ft_residual(ft_plan* p, const double* rhs, const double* u, double* work, double* max_abs_residual,
+                double* max_abs_rhs) {
+    if (!p || !rhs || !u || !max_abs_residual || !max_abs_rhs) return set_err(FT_EINVAL, "ft_residual: bad argument");
+    if (!is_device_ptr(rhs)) return set_err(FT_EINVAL, "ft_residual: device buffers expected");
+    double* y = work;
+    if (!y) {
+        const int rc = ensure_work(p);
+        if (rc) return rc;
+        y = p->work_d;
+    }
+    const int rc = apply_impl(p, u, y);
+    if (rc) return rc;
+    unsigned long long* out = nullptr;
+    FT_CUDA(cudaMalloc(&out, 2 * sizeof(unsigned long long)));
+    cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), p->stream);
+    cudaError_t e = launch_resid_max(y, rhs, rows_of(p) * p->N, out, p->stream);
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(out);
+    if (e != cudaSuccess) return set_err(FT_ECUDA, cudaGetErrorString(e));
+    std::memcpy(max_abs_residual, &h[0], sizeof(double));
+    std::memcpy(max_abs_rhs, &h[1], sizeof(double));
+    return FT_OK;
+}
+
 // diagnostics: the clock64 stamps of the last slab leaf (FT_LEAF_DBG & 4)
 int ft_debug_leaf_clocks(const ft_plan* p, long long* out16) {
     if (!p || !p->dbgclk_d) return set_err(FT_EINVAL, "no leaf clocks");

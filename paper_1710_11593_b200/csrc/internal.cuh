@@ -259,5 +259,8 @@ int gen_terms(const RhsModesArgs& a);  // J of the separable RHS tables
 cudaError_t launch_gen_tables(const RhsModesArgs& a, double* A, double* T, cudaStream_t st);
 cudaError_t launch_toeplitz_matvec(const double* col, const double* row, uint64_t n, const double* x, double* y,
                                    double beta, int block_mode, uint64_t vectors, cudaStream_t st);
+cudaError_t launch_apply_near(const double* x, double* y, uint64_t N, int nodes, uint64_t rows,
+                              const ProblemConst* pc, const double* col, int kind, int L, cudaStream_t st);
+cudaError_t launch_resid_max(const double* y, const double* r, uint64_t n, unsigned long long* out, cudaStream_t st);
 
 }  // namespace ftb
