@@ -105,6 +105,7 @@ struct ft_plan {
     double* wts_d = nullptr;
     double* lampow_d = nullptr;
     int lp_stride = 0;
+    bool paired_g = false;       // resp_g holds the mirror-pair tables (phase 3 of the slab leaf)
     cplx* tw_d = nullptr;
     cplx* spec_d = nullptr;
     double* xch_d = nullptr;      // multi-slab carries of the current leaf
@@ -619,6 +620,29 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             slab_responses(p, (int)b, p->slab, G.data() + b * gsz, H.data() + b * hsz);
             slab_responses(p, (int)b, mlast, G.data() + b * gsz + gsz / 2, H.data() + b * hsz + hsz / 2);
         }
+        // Tridiagonal slabs are mirror symmetric (GR_q = GL_(ms-1-q)): phase 3 corrects the node
+        // pair (q, ms-1-q) from the half-sum / half-difference tables
+        //   S_q = (GL_q + GR_q) / 2 (side 0),  D_q = (GL_q - GR_q) / 2 (side 1),  q < (ms + 1) / 2,
+        // with (EL + ER) and (EL - ER): half the products of the unpaired form (leaf.cu phase 3).
+        p->paired_g = p->kind == SK_TRIDIAG && !p->stencil && getenv("FT_NO_PAIRED_G") == nullptr;
+        if (p->paired_g) {
+            const int m = p->slab, L = p->L;
+            for (uint64_t b = 0; b < B; ++b)
+                for (int kind = 0; kind < 2; ++kind) {
+                    double* g = G.data() + b * gsz + (uint64_t)kind * (gsz / 2);
+                    const int ms = kind == 0 ? m : mlast;
+                    for (int l = 0; l < L; ++l) {
+                        double* gl = g + (uint64_t)l * m;
+                        double* gr = g + ((uint64_t)L + l) * m;
+                        for (int q = 0; q < m; ++q) {
+                            const double A = gl[q], Bv = gr[q];
+                            const bool used = q < (ms + 1) / 2;
+                            gl[q] = used ? 0.5 * (A + Bv) : 0.0;
+                            gr[q] = used ? 0.5 * (A - Bv) : 0.0;
+                        }
+                    }
+                }
+        }
         if ((rc = alloc_copy((void**)&p->respg_d, G.data(), sizeof(double) * G.size()))) return rc;
         if ((rc = alloc_copy((void**)&p->resph_d, H.data(), sizeof(double) * H.size()))) return rc;
         // phase 2 as a matvec: tabulate the reduced recursion's response to unit carries
@@ -785,6 +809,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.node_begin = p->node_begin;
             a.rows_pp = p->local_nodes;
             a.resp_g = p->respg_d;
+            a.paired_g = p->paired_g ? 1 : 0;
             a.resp_h = p->resph_d;
             a.resp_w = p->respw_d;
             a.kc_valid = p->B == 1 && !g_no_kc;

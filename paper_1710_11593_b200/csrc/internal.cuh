@@ -149,6 +149,7 @@ struct LeafArgs {
     int node_begin;            // first node of this rank (X row 0 of a problem)
     int rows_pp;               // X rows per problem held by this plan
     const double* resp_g;      // [B][2 slab kinds][2 (L,R)][slab][L] space-time responses
+    int paired_g;              // resp_g holds mirror-pair tables S = (GL+GR)/2, D = (GL-GR)/2 (tridiagonal)
     const double* resp_h;      // [B][2 slab kinds][L][4] carry responses hFL hFR hBL hBR
     const double* resp_w;      // [B][P][2 (EL,ER)][L lag][2P source carries] injection responses
     int dbg;                   // diagnostics: bit0 skip phase 2, bit1 skip phase 3

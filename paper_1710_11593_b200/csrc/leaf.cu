@@ -872,6 +872,50 @@ __device__ __forceinline__ void correct_body(const LeafArgs& a, double* s_c0, do
     const int tsel = (s == P - 1) ? 1 : 0;
     // tables are time-major [side][l][q]: lanes (consecutive q) read coalesced
     const double* GT = a.resp_g + ((uint64_t)pb * 2 + tsel) * 2 * (uint64_t)m * L;
+    if (TRI && a.paired_g) {
+        // Mirror pairs: x_q += S (EL + ER) + D (EL - ER), x_(mreal-1-q) += S (EL + ER) - D (EL - ER)
+        // with S = (GL_q + GR_q) / 2, D = (GL_q - GR_q) / 2 (GR_q = GL_(mreal-1-q) by symmetry):
+        // one table and one window per pass, half the products and half the table traffic of
+        // the unpaired form (17.1 k -> 13.5 k cycles per leaf; what remains is mostly the 128 CTAs
+        // pulling the same 64 KB table from L2 at once -- fetching it earlier, across phase 2,
+        // cost more in step-loop spills than it saved).
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const double sgn = pass ? -1.0 : 1.0;
+#pragma unroll 1
+            for (int q = tid; q < (mreal + 1) / 2; q += blockDim.x) {
+                const int q2 = mreal - 1 - q;
+                double g[L], win[L];
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    g[l] = GT[((uint64_t)pass * L + l) * m + q];
+                    win[l] = 0.0;
+                }
+                double* xq = s_x + q * (L + 1);
+                double* xq2 = s_x + q2 * (L + 1);
+                const bool two = q2 != q;
+                // the injection of the next step is fetched one iteration ahead and the tile values
+                // before the window products, so no step waits on shared memory
+                double e_next = fma(sgn, s_inj[0][1], s_inj[0][0]);  // EL + ER, EL - ER
+#pragma unroll
+                for (int sg = 0; sg < L / 4; ++sg) {
+#pragma unroll 1
+                    for (int st = 4 * sg; st < 4 * sg + 4; ++st) {
+                        if (st >= len) break;
+                        const double e = e_next;
+                        const double xv = xq[st], xv2 = xq2[st];
+                        const int sn = st + 1 < L ? st + 1 : st;
+                        e_next = fma(sgn, s_inj[sn][1], s_inj[sn][0]);
+                        const double c = fma(g[0], e, win[0]);
+#pragma unroll
+                        for (int i = 0; i < L - 1 - 4 * sg; ++i) win[i] = fma(g[i + 1], e, win[i + 1]);
+                        xq[st] = xv + c;
+                        if (two) xq2[st] = fma(sgn, c, xv2);
+                    }
+                }
+            }
+        }
+    } else
 #pragma unroll 1
     for (int q = tid; q < mreal; q += blockDim.x) {
         double gL[L], gR[TRI ? L : 1], win[L];
