@@ -384,6 +384,20 @@ def run_ours(args, world, rank, local):
         # FT_P2P_EXCHANGE=1: the leaf kernels exchange the carries over NVLink peer memory
         # (ft_p2p_connect) instead of the NCCL hook -- opt-in, not yet run on a multi-GPU box
         plan = ShardedPlan(wl.specs[0], rank, world, device=local, p2p=os.environ.get("FT_P2P_EXCHANGE") == "1")
+        if os.environ.get("FT_P2P_EXCHANGE") != "1" and os.environ.get("FT_NCCL_HOOK") != "1":
+            # the all-gather as ncclAllGather issued by the library (ft_nccl_init): the solve replays
+            # as one CUDA graph; falls back to the torch.distributed hook if NCCL cannot be bound
+            # (every rank takes the same branch: the bind is collective)
+            import torch.distributed as dist
+            ok = torch.ones(1, device=f"cuda:{local}")
+            try:
+                plan.bind_nccl()
+            except Exception as e:  # noqa: BLE001
+                print(f"[rank {rank}] native NCCL exchange unavailable ({e}); using the hook", file=sys.stderr)
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 0:
+                plan = ShardedPlan(wl.specs[0], rank, world, device=local)
         stream = plan.stream
     else:
         # independent problems (config 5: shard the batch) or replicas

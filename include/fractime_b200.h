@@ -160,6 +160,17 @@ int ft_setup_batch(const ft_problem* problems, uint64_t count, const ft_options*
                    ft_plan** out);
 int ft_plan_get_info(const ft_plan* plan, ft_plan_info* info);
 
+/* The carry all-gather as ncclAllGather on the plan's stream, issued by the library itself:
+ * no host callback per leaf, and the whole solve (2048 leaves x {phase-1 kernel, all-gather,
+ * correction kernel} + the history products) is captured into ONE CUDA graph like the
+ * single-GPU solve.  NCCL is bound at run time from the process's libnccl.so.2 (torch's; or
+ * FT_NCCL_LIB) -- no link-time dependency.  Rank 0 calls ft_nccl_unique_id and ships the 128
+ * bytes to every rank by any transport; every rank then calls ft_nccl_init (collective) on its
+ * ft_setup_partitioned plan.  world == 1 is allowed on any wide plan: the same two-kernel leaf
+ * and collective run on one GPU (how the path is tested where only one GPU exists). */
+int ft_nccl_unique_id(void* id128);
+int ft_nccl_init(ft_plan* plan, const void* id128, int rank, int world);
+
 /* Multi-GPU slab partition of one wide problem (BASELINE config 4): rank r of
  * `world` holds the contiguous nodes [node_begin, node_begin + local_nodes)
  * (ft_plan_info); its rhs / u buffers are [local_nodes][N].  History products

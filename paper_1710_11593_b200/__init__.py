@@ -101,7 +101,7 @@ ABI_SYMBOLS = ("ft_setup", "ft_setup_batch", "ft_setup_partitioned", "ft_set_exc
                "ft_assemble_rhs_grid", "ft_assemble_rhs_modes", "ft_solve_fast", "ft_solve_direct",
                "ft_solve_fast_modes", "ft_p2p_handle", "ft_p2p_connect",
                "ft_profile_fast", "ft_schedule", "ft_set_stream", "ft_last_error", "ft_destroy",
-               "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec", "ft_apply", "ft_residual")
+               "ft_setup_toeplitz", "ft_toeplitz_matvec", "ft_block_matvec", "ft_apply", "ft_residual", "ft_nccl_unique_id", "ft_nccl_init")
 
 
 def lib() -> C.CDLL:
@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
         L.ft_solve_fast_modes.argtypes = [P, I, P, P, P, P, P, P, P, C.POINTER(_Report)]
         L.ft_apply.argtypes = [P, P, P]
         L.ft_residual.argtypes = [P, P, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ft_nccl_unique_id.argtypes = [P]
+        L.ft_nccl_init.argtypes = [P, P, I, I]
         L.ft_p2p_handle.argtypes = [P, P]
         L.ft_p2p_connect.argtypes = [P, P]
         L.ft_set_stream.argtypes = [P, P]
@@ -376,6 +378,13 @@ class Plan:
         return [dict(kind=arr[i].kind, level=arr[i].level, t0=arr[i].t0, len=arr[i].len,
                      bytes=arr[i].bytes, ms=arr[i].ms) for i in range(min(cnt.value, cap))]
 
+    def nccl_init(self, unique_id: bytes, rank: int = 0, world: int = 1) -> None:
+        """Bind the per-leaf carry all-gather to ncclAllGather on the plan's stream (collective:
+        every rank calls it with rank 0's `nccl_unique_id()`); the solve then replays as one
+        CUDA graph with the collectives inside."""
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        _check(lib().ft_nccl_init(self._h, buf, rank, world))
+
     def apply(self, x, out=None):
         """y = A x with the plan's system matrix (device tensors; the reference's block
         operator, applied through the plan's FFT history products)."""
@@ -414,6 +423,13 @@ class Plan:
                                          _ptr(out, self.shape[0] * self.shape[1], "u"), C.byref(rep)))
         return out, SolveReport(rep.method.decode(), rep.iterations, rep.residual, rep.seconds,
                                 rep.device_ms, rep.kernel_launches)
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the solver's run-time NCCL binding (rank 0; ship to all ranks)."""
+    buf = (C.c_ubyte * 128)()
+    _check(lib().ft_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def schedule(time_steps: int, leaf: int = 32):
@@ -496,4 +512,4 @@ def l2_error(grid: SolutionGrid, spec: ProblemSpec) -> float:
 
 __all__ = ["FractimeError", "InvalidArgument", "DomainError", "SchemeId", "SolveMethod", "ProblemSpec",
            "SolutionGrid", "SolveReport", "SchemeSolution", "Plan", "solve", "l2_error", "lib",
-           "ABI_SYMBOLS", "FT_RHS_REFERENCE", "FT_RHS_CORRECTED_N1", "schedule"]
+           "nccl_unique_id", "ABI_SYMBOLS", "FT_RHS_REFERENCE", "FT_RHS_CORRECTED_N1", "schedule"]

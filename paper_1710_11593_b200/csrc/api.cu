@@ -3,6 +3,7 @@
 // no FMA contraction in host code), device-resident plan, and the
 // divide-and-conquer driver.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -52,6 +53,41 @@ struct Op {
     bool first;    // reads R from the caller's rhs (first touch)
 };
 
+// NCCL, bound at run time from the library the process already has (torch's libnccl.so.2) so
+// the solver has no link-time dependency on it: only the calls the carry all-gather needs.
+struct NcclId {
+    char bytes[128];  // ncclUniqueId
+};
+struct NcclApi {
+    int (*GetUniqueId)(NcclId*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+    int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+    bool ok = false;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        const char* names[] = {getenv("FT_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) {
+            if (!n) continue;
+            void* h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (!h) continue;
+            a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+            a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+            a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+            a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+            a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+            a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+            if (a.ok) break;
+        }
+        return a;
+    }();
+    return api;
+}
+constexpr int kNcclFloat64 = 8;  // ncclDataType_t ncclFloat64 / ncclDouble
+
 }  // namespace
 
 struct ft_plan {
@@ -85,6 +121,7 @@ struct ft_plan {
     double* xsend_d = nullptr;  // caller-provided (partitioned) phase-1 carry buffer
     bool own_xch = true;
     // device-side exchange over NVLink peer memory (ft_p2p_handle / ft_p2p_connect)
+    void* nccl_comm = nullptr;                 // ft_nccl_init: the carry all-gather is ncclAllGather on the plan's stream
     bool p2p = false;
     void* p2p_block = nullptr;                 // this rank's exchange block (kP2pHeader + receive buffers)
     std::vector<void*> p2p_opened;             // peers' blocks mapped through CUDA IPC
@@ -852,9 +889,13 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
                 FT_CUDA(launch_leaf(p->kind, p->npt, p->L, p->multi, a, p->B * p->P_local, p->threads, st));
             }
             if (p->multi && !p->p2p && !(p->part_world == 1 && p->fused_leaf)) {
-                if (p->part_world > 1) {  // one carry all-gather per leaf (caller's collective)
+                if (p->nccl_comm) {  // one carry all-gather per leaf: NCCL on the plan's stream (graph-capturable)
+                    const int nr = nccl_api().AllGather(p->xsend_d, p->xch_d, (size_t)p->P_local * p->L * 2,
+                                                        kNcclFloat64, p->nccl_comm, st);
+                    if (nr) return set_err(FT_ESOLVER, std::string("ncclAllGather: ") + nccl_api().GetErrorString(nr));
+                } else if (p->part_world > 1) {  // the caller's collective
                     if (!p->exchange)
-                        return set_err(FT_EINVAL, "partitioned plan: no exchange hook (ft_set_exchange)");
+                        return set_err(FT_EINVAL, "partitioned plan: no exchange hook (ft_set_exchange / ft_nccl_init)");
                     const int rc = p->exchange(p->exchange_user, (uint64_t)p->P_local * p->L * 2, (void*)st);
                     if (rc) return set_err(FT_ESOLVER, "partitioned plan: exchange hook failed");
                 }
@@ -1068,6 +1109,55 @@ int ft_p2p_connect(ft_plan* p, const void* handles) {
     p->p2p = true;
     if (p->graph) cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
+    return FT_OK;
+}
+
+int ft_nccl_unique_id(void* id128) {
+    if (!id128) return set_err(FT_EINVAL, "ft_nccl_unique_id: null argument");
+    if (!nccl_api().ok) return set_err(FT_ESOLVER, "NCCL not found (libnccl.so.2; set FT_NCCL_LIB)");
+    NcclId id;
+    const int nr = nccl_api().GetUniqueId(&id);
+    if (nr) return set_err(FT_ESOLVER, std::string("ncclGetUniqueId: ") + nccl_api().GetErrorString(nr));
+    std::memcpy(id128, id.bytes, sizeof(id.bytes));
+    return FT_OK;
+}
+
+int ft_nccl_init(ft_plan* p, const void* id128, int rank, int world) {
+    if (!p || !id128) return set_err(FT_EINVAL, "ft_nccl_init: null argument");
+    if (!p->multi) return set_err(FT_EINVAL, "ft_nccl_init: the plan has no slab leaf (a single slab needs no exchange)");
+    if (world != p->part_world || rank != p->part_rank)
+        return set_err(FT_EINVAL, "ft_nccl_init: rank / world differ from the plan's partition");
+    if (p->B != 1) return set_err(FT_EINVAL, "ft_nccl_init: single-problem plans only");
+    if (p->p2p) return set_err(FT_EINVAL, "ft_nccl_init: the plan already exchanges over peer memory");
+    if (!nccl_api().ok) return set_err(FT_ESOLVER, "NCCL not found (libnccl.so.2; set FT_NCCL_LIB)");
+    FT_CUDA(cudaSetDevice(p->device));
+    if (p->nccl_comm) {
+        nccl_api().CommDestroy(p->nccl_comm);
+        p->nccl_comm = nullptr;
+    }
+    NcclId id;
+    std::memcpy(id.bytes, id128, sizeof(id.bytes));
+    void* comm = nullptr;
+    const int nr = nccl_api().CommInitRank(&comm, world, id, rank);
+    if (nr) return set_err(FT_ESOLVER, std::string("ncclCommInitRank: ") + nccl_api().GetErrorString(nr));
+    p->nccl_comm = comm;
+    // in-place all-gather: this rank's phase-1 carries go straight into its block of the
+    // gathered array (the plan's own buffer, [P][L][2], rank-major = slab-major)
+    if (!p->own_xch) {
+        p->xch_d = nullptr;
+        const int rc = alloc_copy((void**)&p->xch_d, nullptr, sizeof(double) * 2 * 2 * p->B * p->P * p->L);
+        if (rc) return rc;
+        p->own_xch = true;
+    }
+    p->xsend_d = p->xch_d + (size_t)rank * p->P_local * p->L * 2;
+    p->exchange = nullptr;
+    // the collective sits between phase 1 and the correction: two kernels per leaf (also for
+    // world = 1, which exercises this path on one GPU)
+    p->fused_leaf = false;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
     return FT_OK;
 }
 
@@ -1339,7 +1429,7 @@ static int launch_fast(ft_plan* p, double* X, const double* src, const GenRhs* g
         *launches = 1;
         return FT_OK;
     }
-    const bool use_graph = (p->part_world == 1 || p->p2p) && !getenv("FT_NO_GRAPH");
+    const bool use_graph = (p->part_world == 1 || p->p2p || p->nccl_comm) && !getenv("FT_NO_GRAPH");
     if (!use_graph) return run_fast(p, X, src, launches, nullptr, nullptr, gen);
     const void* gkey = gen ? (const void*)gen->A : nullptr;
     const int gJ = gen ? gen->J : 0;
@@ -1795,6 +1885,7 @@ void ft_destroy(ft_plan* p) {
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->nccl_comm) nccl_api().CommDestroy(p->nccl_comm);
     if (p->rdev_d) cudaFree(p->rdev_d);
     for (void* q : p->p2p_opened) cudaIpcCloseMemHandle(q);
     if (p->p2p_block) cudaFree(p->p2p_block);

@@ -81,7 +81,7 @@ class ShardedPlan(Plan):
     `self.send` into `self.recv` on `self.stream`."""
 
     def __init__(self, spec, rank: int, world: int, exchange_factory=None, device: int = -1, p2p: bool = False,
-                 **kw):
+                 native_nccl: bool = False, **kw):
         super().__init__(spec, partition=(rank, world), device=device, **kw)
         self.rank, self.world = rank, world
         P_local, L = int(self.info.slabs_local), int(self.info.leaf)
@@ -107,6 +107,21 @@ class ShardedPlan(Plan):
         _check(lib().ft_set_exchange(self._h, self._hook, None, self.send.data_ptr(), self.recv.data_ptr()))
         if p2p:
             self.connect_peers()
+        elif native_nccl:
+            self.bind_nccl()
+
+    def bind_nccl(self, group=None) -> None:
+        """The carry all-gather as ncclAllGather issued by the library on the plan's stream
+        (ft_nccl_init): rank 0's unique id is broadcast over torch.distributed (any backend),
+        every rank joins the solver's own communicator; solves then replay as one CUDA graph."""
+        import torch.distributed as dist
+
+        from . import nccl_unique_id
+
+        box = [nccl_unique_id() if self.rank == 0 else None]
+        if self.world > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        self.nccl_init(box[0], self.rank, self.world)
 
     def connect_peers(self, group=None) -> None:
         """Switch to the in-kernel exchange over NVLink peer memory: all-gather the

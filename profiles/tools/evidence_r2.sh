@@ -23,7 +23,8 @@ cap() {  # name kernel-regex launch-skip [prof args]
   ncu -i /tmp/ncu/cap_$name.ncu-rep --page source --csv --print-source sass > /tmp/ncu/cap_${name}_sass.csv 2>/dev/null
   gzip -c /tmp/ncu/cap_${name}_sass.csv > $O/cap_${name}_sass.csv.gz
 }
-cap leaf_fused "leaf_fused" 100
+cap leaf_pair "leaf_pair" 100
+FT_NO_PAIR=1 cap leaf_fused "leaf_fused" 100
 cap split16 "mp_split_kernel<.int.16" 0
 cap split8 "mp_split_kernel<.int.8," 0
 cap cluster2 "mp_kernel<.int.2," 0
@@ -34,5 +35,5 @@ cap direct64 "mp_direct_kernel" 300
 cap ode_whole "ode_whole_kernel" 0 --config 1
 cap leaf_cfg2 "leaf_kernel" 60 --config 2
 cap leaf_cfg3 "leaf_fused" 60 --config 3 --time-steps 8192
-cp /tmp/ncu/cap_leaf_fused.ncu-rep /tmp/ncu/cap_split16.ncu-rep $O/ 2>/dev/null
+cp /tmp/ncu/cap_leaf_pair.ncu-rep /tmp/ncu/cap_split16.ncu-rep $O/ 2>/dev/null
 du -sh $O

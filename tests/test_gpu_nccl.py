@@ -1,0 +1,47 @@
+"""The carry all-gather as ncclAllGather issued by the library (ft_nccl_init), captured with the
+rest of the solve into one CUDA graph.  Every GPU tier of this run has one GPU, so the path is
+exercised with a one-rank communicator: the same two-kernel leaf (phase 1 / all-gather /
+correction), the same buffers and the same graph capture as on N ranks; the slab partition itself
+is covered across 2 and 4 processes by tests/test_parallel.py (gloo exchange)."""
+import pytest
+
+from paper_1710_11593_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cid,kw", [(4, dict(time_steps=1024, cells=2049)),      # 5 slabs, ragged last
+                                    (3, dict(time_steps=512, cells=1025))],     # wave scheme, 2 slabs
+                         ids=["diffusion-5-slabs", "wave-2-slabs"])
+def test_native_nccl_exchange_one_rank(ft, cid, kw):
+    import torch
+
+    w = W.config(cid, **kw)
+    plan = ft.Plan(w.specs)
+    R = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    U0, rep0 = plan.solve_fast(R)
+    try:
+        uid = ft.nccl_unique_id()
+    except ft.FractimeError as e:
+        pytest.skip(f"NCCL not loadable here: {e}")
+    plan2 = ft.Plan(w.specs)
+    plan2.nccl_init(uid, 0, 1)
+    U1, rep1 = plan2.solve_fast(R)
+    U2, rep2 = plan2.solve_fast(R)   # graph replay with the collectives inside
+    assert torch.equal(U1, U0) and torch.equal(U2, U0)
+    leaves = (plan.N + 31) // 32
+    # two kernels per leaf (the collective between them) instead of one cooperative kernel
+    assert rep1.kernel_launches >= 2 * leaves and rep1.kernel_launches == rep2.kernel_launches
+    assert rep1.kernel_launches > rep0.kernel_launches
+
+
+def test_nccl_init_rejects_bad_arguments(ft):
+    w = W.config(2, time_steps=64, cells=17)      # single slab: nothing to exchange
+    plan = ft.Plan(w.specs)
+    with pytest.raises(ft.InvalidArgument):
+        plan.nccl_init(bytes(128), 0, 1)
+    w = W.config(4, time_steps=64, cells=1025)
+    plan = ft.Plan(w.specs)
+    with pytest.raises(ft.InvalidArgument):
+        plan.nccl_init(bytes(128), 1, 2)          # not this plan's partition
