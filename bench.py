@@ -60,8 +60,9 @@ def peaks():
 # (profiles/ncu_r02/fp64_dram_per_launch_cfg4.csv.gz, summarised in DESIGN.md §4):
 # direct n <= 128: 0.68, single-CTA FFT 256 <= n <= 4096: 0.92, 2-/4-CTA clusters
 # (n = 8192, 16384): 1.00, persistent split levels (n >= 32768, their scratch ring
-# partly spilling to DRAM): 2.71.
-NCU_DRAM_OVER_ALG = {"direct": 0.68, "single": 0.92, "cluster": 1.00, "split": 2.71}
+# partly spilling to DRAM; dead ring lines discarded from L2): 1.29 (n = 65536: 1.49,
+# n = 32768: 1.09; round 1's batched launches: 2.71).
+NCU_DRAM_OVER_ALG = {"direct": 0.68, "single": 0.92, "cluster": 1.00, "split": 1.29}
 
 
 def mp_family(n: int) -> str:

@@ -13,10 +13,13 @@ ap.add_argument("--time-steps", type=int, default=0)
 ap.add_argument("--cells", type=int, default=0)
 ap.add_argument("--solves", type=int, default=3)
 ap.add_argument("--split", action="store_true")
+ap.add_argument("--nccl", action="store_true", help="one-rank NCCL exchange (two-kernel leaf + ncclAllGather in the graph)")
 ap.add_argument("--check", type=int, default=0, help="parity vs ft_solve_direct on this many steps (0: off)")
 a = ap.parse_args()
 wl = W.config(a.config, time_steps=a.time_steps or None, cells=a.cells or None)
 plan = ft.Plan(wl.specs, device=0)
+if a.nccl:
+    plan.nccl_init(ft.nccl_unique_id(), 0, 1)
 rhs = torch.empty(plan.shape, dtype=torch.float64, device="cuda"); u = torch.empty_like(rhs)
 plan.assemble_rhs_modes(rhs, wl.a, wl.k, wl.p, wl.trig, wl.u0amp, wl.phiamp)
 ms = []

@@ -13,7 +13,12 @@ LIB = os.path.join(os.path.dirname(__file__), "..", "..", "paper_1710_11593_b200
 KERNELS = {
     "mp_split_kernel_16": r"_ZN3ftb15mp_split_kernelILi16ELi12EEEvNS_6MpArgsENS_6SplitQE",
     "mp_split_kernel_8": r"_ZN3ftb15mp_split_kernelILi8ELi12EEEvNS_6MpArgsENS_6SplitQE",
-    "leaf_fused_tridiag": r"_ZN3ftb10leaf_fusedILi2ELi2ELi32ELb1EEEvNS_8LeafArgsE",
+    "leaf_pair_tridiag": r"_ZN3ftb9leaf_pairILi2ELi2ELi32EEEvNS_8LeafArgsE",
+    "leaf_fused_tridiag": r"_ZN3ftb10leaf_fusedILi2ELi2ELi32ELb1ELb1EEEvNS_8LeafArgsE",
+    "mp1g_kernel_9": r"_ZN3ftb11mp1g_kernelILi9EEEvNS_6MpArgsE",
+    "mp1p_kernel_12_tma": r"_ZN3ftb11mp1p_kernelILi12EEEvNS_6MpArgsEi",
+    "mp8_kernel_9_radix8": r"_ZN3ftb10mp8_kernelILi9EEEvNS_6MpArgsE",
+    "mp_direct_kernel_64": r"_ZN3ftb16mp_direct_kernelILi64EEEvNS_6MpArgsE",
     "mp1g_kernel_12": r"_ZN3ftb11mp1g_kernelILi12EEEvNS_6MpArgsE",
     "mp_kernel_cluster4": r"_ZN3ftb9mp_kernelILi4ELi12ELb0ELb0EEEvNS_6MpArgsE",
     "direct_multi_kernel": r"_ZN3ftb19direct_multi_kernelENS_10DirectArgsEPjii",
