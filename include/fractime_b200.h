@@ -227,8 +227,8 @@ int ft_solve_direct(ft_plan* plan, const double* rhs, double* u, ft_report* repo
  * embedding :84-115) and the matrix ft_solve_fast inverts.  The far history runs through the
  * plan's own FFT / direct history products (O(M N log N), the level spectra cached at setup);
  * the in-leaf lags and the spatial stencil are added in the difference form
- * (d - 2b) x_i - b ((x_(i-1) - x_i) + (x_(i+1) - x_i)).  x, y: distinct device buffers,
- * [rows][N].  Scheme 2 and partitioned plans: FT_EINVAL. */
+ * (d - 2b) x_i - b ((x_(i-1) - x_i) + (x_(i+1) - x_i)).  x, y: distinct buffers [rows][N], both
+ * on the device or both on the host (staged).  Scheme 2 and partitioned plans: FT_EINVAL. */
 int ft_apply(ft_plan* plan, const double* x_device, double* y_device);
 /* max |A u - rhs| and max |rhs| over all unknowns (the reference's SolveReport::residual is
  * GMRES's; the D&C is direct, so ft_solve_fast reports 0 and this call measures it).  work:

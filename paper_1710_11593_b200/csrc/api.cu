@@ -1720,7 +1720,7 @@ static int apply_impl(ft_plan* p, const double* x, double* y) {
     if (p->stencil) return set_err(FT_EINVAL, "ft_apply: Scheme 2 (stencil history) plans are not supported");
     if (p->part_world != 1) return set_err(FT_EINVAL, "ft_apply: partitioned plans are not supported");
     if (!is_device_ptr(x) || !is_device_ptr(y) || x == y)
-        return set_err(FT_EINVAL, "ft_apply: x and y must be distinct device buffers");
+        return set_err(FT_EINVAL, "ft_apply: x and y must be distinct buffers, both on the device or both on the host");
     FT_CUDA(cudaSetDevice(p->device));
     cudaStream_t st = p->stream;
     const uint64_t N = p->N;
@@ -1759,6 +1759,27 @@ static int apply_impl(ft_plan* p, const double* x, double* y) {
 }
 
 int ft_apply(ft_plan* p, const double* x, double* y) {
+    if (p && x && y && !is_device_ptr(x) && !is_device_ptr(y)) {
+        // host vectors (the reference's LinearOperator::apply takes and returns host spans):
+        // staged through two device buffers
+        FT_CUDA(cudaSetDevice(p->device));
+        const size_t bytes = sizeof(double) * rows_of(p) * p->N;
+        double *xd = nullptr, *yd = nullptr;
+        if (cudaMalloc(&xd, bytes) != cudaSuccess || cudaMalloc(&yd, bytes) != cudaSuccess) {
+            cudaFree(xd);
+            return set_err(FT_ENOMEM, "ft_apply: device staging buffers");
+        }
+        cudaError_t e = cudaMemcpyAsync(xd, x, bytes, cudaMemcpyHostToDevice, p->stream);
+        int rc = e == cudaSuccess ? apply_impl(p, xd, yd) : set_err(FT_ECUDA, cudaGetErrorString(e));
+        if (!rc) {
+            e = cudaMemcpyAsync(y, yd, bytes, cudaMemcpyDeviceToHost, p->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+            if (e != cudaSuccess) rc = set_err(FT_ECUDA, cudaGetErrorString(e));
+        }
+        cudaFree(xd);
+        cudaFree(yd);
+        return rc;
+    }
     const int rc = apply_impl(p, x, y);
     if (rc) return rc;
     FT_CUDA(cudaStreamSynchronize(p->stream));

@@ -91,6 +91,16 @@ LinearOperator make_toeplitz_operator_b200(const ToeplitzOperator& t) {
                           }};
 }
 
+// The reference's make_block_operator (toeplitz.cpp:194-197) on the plan's own matrix: the far
+// history through the plan's FFT history products (ft_apply), host spans in and out.
+LinearOperator make_block_operator_b200(ft_plan* plan, std::size_t dim) {
+    return LinearOperator{dim, [plan](std::span<const double> x) {
+                              std::vector<double> y(x.size());
+                              check(ft_apply(plan, x.data(), y.data()));
+                              return y;
+                          }};
+}
+
 // ---------------- the checks ----------------
 static double relerr(const std::vector<double>& a, const std::vector<double>& b) {
     double num = 0.0, den = 0.0;
@@ -176,6 +186,36 @@ int main() {
         std::vector<double> yg(xb.size());
         check(ft_block_matvec(col.data(), T.first_row().data(), n, 7, -3.5, xb.data(), yg.data()));
         expect(relerr(yg, yr) <= 1e-13, "block matvec GPU vs reference", relerr(yg, yr));
+
+        // 7: the reference's own Scheme 4 fast path (schemes.cpp:464-474: assemble_scheme4 +
+        //    make_block_operator + gmres_solve) with the block operator replaced by the plan's
+        //    GPU operator: same Krylov solver, same right-hand side, same answer
+        {
+            ProblemSpec s7 = s4;
+            s7.time_steps = 96;     // three leaves: n = 64 and n = 128 products + in-leaf lags
+            s7.space_cells = 13;
+            const auto system = assemble_scheme4(s7);
+            ft_problem p7{FT_SCHEME_DIFFUSION, s7.gamma, s7.time_steps, s7.space_cells, s7.time_length, s7.space_length};
+            ft_plan* plan7 = nullptr;
+            check(ft_setup(&p7, nullptr, &plan7));
+            const auto gpu_block = make_block_operator_b200(plan7, system.rhs.size());
+            const auto ref_block = make_block_operator(system.op);
+            std::vector<double> xp(system.rhs.size());
+            for (size_t i = 0; i < xp.size(); ++i) xp[i] = std::sin(0.37 * (double)i) + 0.01 * (double)(i % 7);
+            const auto ag = gpu_block.apply(xp), ar = ref_block.apply(xp);
+            expect(relerr(ag, ar) <= 1e-12, "block operator: ft_apply vs reference block_matvec", relerr(ag, ar));
+            SolverConfig c7;
+            c7.tol = 1e-11;
+            c7.restart = 60;
+            c7.max_iter = 20000;
+            const auto g7 = gmres_solve(gpu_block, system.rhs, c7);
+            const auto d7 = solve(s7, SolveMethod::Direct, SolverConfig{});
+            expect(g7.converged, "reference gmres on the plan's GPU block operator converged (matvecs)",
+                   (double)g7.iterations);
+            expect(relerr(g7.solution, d7.grid.values) <= 1e-8, "gmres(GPU block op) vs reference direct",
+                   relerr(g7.solution, d7.grid.values));
+            ft_destroy(plan7);
+        }
 
         // 6: error mapping (validate: gamma out of range -> invalid_argument)
         bool threw = false;

@@ -4,7 +4,8 @@ reference's own headers and linked with the unmodified reference library
 __graft_entry__.build()).  On the GPU the program drives the reference's
 solve() / gmres_solve() next to the B200 entry points (section 1: solve_scheme4_b200 /
 solve_scheme3_b200 with std::function callbacks through ft_assemble_rhs; section 5:
-the reference GMRES on the GPU LinearOperator)."""
+the reference GMRES on the GPU LinearOperator; the reference's Scheme 4 fast path -- assemble_scheme4 +
+gmres_solve -- on the plan's own GPU block operator, ft_apply)."""
 import subprocess
 from pathlib import Path
 
@@ -33,4 +34,4 @@ def test_binding_runs_reference_api_on_gpu():
     print(r.stdout)
     lines = [line for line in r.stdout.splitlines() if line.strip()]
     assert r.returncode == 0, r.stdout + r.stderr
-    assert len(lines) >= 11 and all(line.startswith("ok ") for line in lines), r.stdout
+    assert len(lines) >= 14 and all(line.startswith("ok ") for line in lines), r.stdout
