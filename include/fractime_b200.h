@@ -275,7 +275,10 @@ int ft_setup_toeplitz(const double* first_cols, uint64_t n, uint64_t count, cons
  * (src/toeplitz.cpp:84-115); computed as a direct fp64 product on the GPU (no
  * circulant rounding).  first_col[0] != first_row[0] -> FT_EINVAL with the
  * reference's message (src/toeplitz.cpp:31-32).  All arrays host or device;
- * x == y allowed. */
+ * x == y allowed.  O(n^2) per vector and no setup: meant for one-off products.  A lower
+ * triangular operator applied many times (a Krylov loop) should use a Toeplitz plan instead:
+ * ft_setup_toeplitz caches the level spectra once and ft_apply(plan, x, y) runs the FFT
+ * history products, O(n log n) per vector. */
 int ft_toeplitz_matvec(const double* first_col, const double* first_row, uint64_t n, uint64_t count,
                        const double* x, double* y);
 

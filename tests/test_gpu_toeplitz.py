@@ -78,3 +78,21 @@ def test_toeplitz_errors(ft):
     plan = ft.Plan.toeplitz(np.array([2.0, 1.0]))
     with pytest.raises(ft.InvalidArgument, match="no scheme"):
         plan.assemble_rhs_grid(np.zeros((1, 2)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,count", [(1000, 3), (65536, 2)])
+def test_toeplitz_plan_apply_is_the_fft_matvec(ft, oracle_mod, n, count):
+    """The O(n log n) route of toeplitz_matvec (embed_circulant + FFT, toeplitz.cpp:84-115) for
+    lower-triangular operators applied many times: a Toeplitz plan (ft_setup_toeplitz) caches the
+    level spectra and ft_apply runs the FFT history products.  Against the direct O(n^2) GPU
+    product, which test_toeplitz_matvec pins to the oracle."""
+    import torch
+
+    cols = np.stack([oracle_mod.toeplitz_case(n, n + b, True)[0] for b in range(count)])
+    X = np.random.default_rng(n).standard_normal((count, n))
+    plan = ft.Plan.toeplitz(cols)
+    Y = plan.apply(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = np.stack([ft.toeplitz_matvec(cols[b], X[b:b + 1])[0] for b in range(count)])
+    scale = np.abs(cols).sum(axis=1).max() * np.abs(X).max()
+    assert np.max(np.abs(Y - ref)) <= 1e-13 * scale
