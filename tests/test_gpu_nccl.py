@@ -45,3 +45,20 @@ def test_nccl_init_rejects_bad_arguments(ft):
     plan = ft.Plan(w.specs)
     with pytest.raises(ft.InvalidArgument):
         plan.nccl_init(bytes(128), 1, 2)          # not this plan's partition
+
+
+def test_fast_solve_is_bitwise_reproducible(ft):
+    """Repeated solves (CUDA-graph replays) and a second plan give identical bits: every output
+    is written by exactly one task in a fixed summation order -- including the split levels,
+    whose fold / branch / combine tasks are handed out by a dynamic queue (n = 32768, 65536)."""
+    import torch
+
+    w = W.config(4, cells=1537)                      # 3 slabs, full N = 65536: every level incl. split K = 8, 16
+    plan = ft.Plan(w.specs)
+    R = torch.empty(plan.shape, dtype=torch.float64, device="cuda")
+    plan.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    U1, _ = plan.solve_fast(R)
+    U2, _ = plan.solve_fast(R, torch.empty_like(R))
+    plan2 = ft.Plan(w.specs)
+    U3, _ = plan2.solve_fast(R)
+    assert torch.equal(U1, U2) and torch.equal(U1, U3)
