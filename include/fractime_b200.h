@@ -34,6 +34,14 @@
  *                                 (make_toeplitz_operator, src/toeplitz.cpp:198-201)
  *   ft_block_matvec            <- BlockTridiagonalToeplitzOperator + block_matvec()
  *                                 src/toeplitz.cpp:117-167 (make_block_operator :203-208)
+ *   ft_apply / ft_residual     <- make_block_operator() / make_toeplitz_operator() on the plan's own
+ *                                 matrix (src/toeplitz.cpp:194-208: the operator the fast path's
+ *                                 gmres_solve applies, src/schemes.cpp:464-474), through the plan's
+ *                                 FFT history products; SolveReport::residual of a finished solve
+ *   ft_setup_partitioned,      <- (no reference counterpart: the reference is single-process) slab
+ *   ft_set_exchange,              partition of one wide problem over the GPUs of a node, the carry
+ *   ft_nccl_*, ft_p2p_*           all-gather per leaf by the caller's collective, by ncclAllGather
+ *                                 inside the captured graph, or by NVLink peer stores
  *   ft_last_error              <- the what() of the reference's std::exception
  *
  * Conventions
