@@ -285,6 +285,12 @@ def run_reference_arm(args, world, rank):
     if not args.no_configs and args.config == 4:
         for cid in (1, 2, 3, 5):
             subs[f"cfg{cid}"] = reference_estimate(cid)
+        # config 2 is the one multi-node config whose full direct solve the reference finishes in
+        # under a minute: measured once at full size next to the reduced-M estimate (checks the law)
+        t_full, kind = _ref_one(W.config(2))
+        subs["cfg2"]["full_direct_measured_s"] = t_full
+        subs["cfg2"]["full_direct_measured_value"] = W.config(2).unknowns / t_full
+        subs["cfg2"]["law_over_measured"] = subs["cfg2"]["full_solve_s"] / t_full
     line = {
         "impl": "reference",
         "metric": METRIC,
