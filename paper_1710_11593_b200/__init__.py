@@ -386,10 +386,10 @@ class Plan:
         _check(lib().ft_nccl_init(self._h, buf, rank, world))
 
     def apply(self, x, out=None):
-        """y = A x with the plan's system matrix (device tensors; the reference's block
-        operator, applied through the plan's FFT history products)."""
+        """y = A x with the plan's system matrix (the reference's block operator, applied
+        through the plan's FFT history products); x, out: both device tensors or both host arrays."""
         if out is None:
-            out = x.new_empty(self.shape)
+            out = np.empty(self.shape) if isinstance(x, np.ndarray) else x.new_empty(self.shape)
         n = self.shape[0] * self.shape[1]
         self._check_device(x, "x")
         self._check_device(out, "y")

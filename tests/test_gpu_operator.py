@@ -58,6 +58,7 @@ def test_apply_matches_dense_operator(ft, cid, kw):
     ref = _dense_apply(plan, w, x)
     err = np.abs(y - ref).max() / np.abs(ref).max()
     assert err <= 1e-12, f"rel err {err:.3e}"
+    assert np.array_equal(plan.apply(x), y)      # host arrays in and out (staged): same bits
 
 
 ROUND_TRIPS = [
