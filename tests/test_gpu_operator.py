@@ -135,3 +135,61 @@ def test_apply_rejects_unsupported(ft):
     x = torch.zeros(plan.shape, dtype=torch.float64, device="cuda")
     with pytest.raises(ft.InvalidArgument):
         plan.apply(x, x)
+
+
+@pytest.mark.parametrize("cid,kw", [(1, dict(time_steps=300)), (2, dict(time_steps=200, cells=33)),
+                                    (3, dict(time_steps=200, cells=700)), (4, dict(time_steps=128, cells=1100))],
+                         ids=["ode", "diffusion", "wave-2-slabs", "diffusion-3-slabs"])
+def test_homogeneous_problem_gives_zero(ft, cid, kw):
+    """Zero right-hand side -> exactly zero solution on both paths (reference
+    test_schemes.cpp:268-272 'homogeneous problems give 0')."""
+    import torch
+
+    w = W.config(cid, **kw)
+    plan = ft.Plan(w.specs)
+    R = torch.zeros(plan.shape, dtype=torch.float64, device="cuda")
+    Uf, _ = plan.solve_fast(R)
+    Ud, _ = plan.solve_direct(R)
+    assert torch.count_nonzero(Uf).item() == 0 and torch.count_nonzero(Ud).item() == 0
+
+
+@pytest.mark.parametrize("scheme,cells,steps", [(3, 9, 16), (3, 17, 12), (2, 9, 16)],
+                         ids=["diffusion-8x16", "diffusion-16x12", "wave-8x16"])
+def test_operator_entries_equal_time_marching_matrix(ft, scheme, cells, steps):
+    """The reference's permutation-equivalence criterion (test_schemes.cpp:226-257, acceptance
+    criterion 7, M, N <= 16): the node-major block operator equals, entry by entry, the stacked
+    time-marching matrix -- row (i, n) holds col[n - k] at (i, k), k <= n, and the stencil at the
+    neighbours (i +- 1, n).  The operator's columns come from ft_apply on unit vectors (all lags
+    are in-leaf at N <= 16: single products, exact)."""
+    import torch
+
+    from paper_1710_11593_b200 import ProblemSpec, SchemeId
+
+    s = ProblemSpec(SchemeId(scheme), 0.6 if scheme == 3 else 1.5, steps, cells, 1.0, 1.0)
+    plan = ft.Plan([s])
+    M, N = plan.shape
+    col = plan.column(0)
+    h = s.h()
+    A = np.zeros((M * N, M * N))
+    for i in range(M):
+        for n in range(N):
+            r = i * N + n
+            for k in range(n + 1):
+                A[r, i * N + k] = col[n - k]
+            if scheme == 3:
+                if i > 0:
+                    A[r, (i - 1) * N + n] = -1.0 / (h * h)
+                if i + 1 < M:
+                    A[r, (i + 1) * N + n] = -1.0 / (h * h)
+            elif i > 0:
+                A[r, (i - 1) * N + n] = -1.0 / h
+    E = torch.eye(M * N, dtype=torch.float64, device="cuda")
+    got = np.empty_like(A)
+    for c in range(M * N):
+        got[:, c] = plan.apply(E[c].reshape(M, N).contiguous()).reshape(-1).cpu().numpy()
+    # the stencil is applied in the difference form (d - 2b) x - b ((xl - x) + (xr - x)): on a unit
+    # vector the diagonal entry is re-formed as (d - 2b) + 2b (or (d - s) + s), exact up to one rounding
+    off = ~np.eye(M * N, dtype=bool)
+    assert np.array_equal(got[off], A[off])
+    d = np.abs(np.diag(got) - np.diag(A)) / np.abs(np.diag(A))
+    assert d.max() <= 2.3e-16
