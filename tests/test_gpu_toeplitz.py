@@ -96,3 +96,53 @@ def test_toeplitz_plan_apply_is_the_fft_matvec(ft, oracle_mod, n, count):
     ref = np.stack([ft.toeplitz_matvec(cols[b], X[b:b + 1])[0] for b in range(count)])
     scale = np.abs(cols).sum(axis=1).max() * np.abs(X).max()
     assert np.max(np.abs(Y - ref)) <= 1e-13 * scale
+
+
+@pytest.mark.gpu
+def test_random_toeplitz_operators_vs_dense(ft):
+    """The reference's randomized operator checks (test_fft_toeplitz.cpp:76-103: 40 random
+    Toeplitz matvecs, seed 42, 1e-13; acceptance criterion 2: 200 operators, seed 2024, 1e-12):
+    200 random general Toeplitz operators of random size against the dense product."""
+    rng = np.random.default_rng(2024)
+    worst = 0.0
+    for _ in range(200):
+        n = int(rng.integers(1, 400))
+        col = rng.standard_normal(n)
+        row = rng.standard_normal(n)
+        row[0] = col[0]
+        x = rng.standard_normal((1, n))
+        i, j = np.indices((n, n))
+        T = np.where(i >= j, col[np.abs(i - j)], row[np.abs(i - j)])
+        y = ft.toeplitz_matvec(col, x, row)[0]
+        ref = T @ x[0]
+        worst = max(worst, np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-300))
+    assert worst <= 1e-12, worst
+
+
+@pytest.mark.gpu
+def test_plan_apply_scales_like_n_log_n(ft, oracle_mod):
+    """The reference's complexity criterion for the FFT matvec (acceptance criterion 8: time
+    ratio <= 2.6 per doubling of n, acceptance.cpp:293-348), on the plan route (ft_apply on a
+    Toeplitz plan, 128 vectors at once), n = 16384 -> 32768 -> 65536."""
+    import torch
+
+    times = []
+    for n in (16384, 32768, 65536):
+        cols = np.tile(oracle_mod.toeplitz_case(n, 5, True)[0], (128, 1))
+        plan = ft.Plan.toeplitz(cols)
+        x = torch.randn(plan.shape, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        plan.apply(x, y)
+        reps = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            plan.apply(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            reps.append(e0.elapsed_time(e1))
+        times.append(sorted(reps)[2])
+        del plan, x, y
+    print("ft_apply ms at n = 16384, 32768, 65536 (128 vectors):", times)
+    assert times[1] / times[0] <= 2.6 and times[2] / times[1] <= 2.6, times
