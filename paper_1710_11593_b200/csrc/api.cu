@@ -169,6 +169,9 @@ struct ft_plan {
     const void* graph_src = nullptr;
     const void* graph_gen = nullptr;
     int graph_genJ = 0;
+    cudaGraphExec_t apply_graph = nullptr;  // ft_apply's launch sequence, keyed by its buffers
+    const void* apply_x = nullptr;
+    const void* apply_y = nullptr;
     double* genA_d = nullptr;     // ft_solve_fast_modes tables
     double* genT_d = nullptr;
     size_t genA_bytes = 0, genT_bytes = 0;
@@ -1715,6 +1718,7 @@ int ft_solve_fast_modes(ft_plan* p, int nmodes, const double* a, const double* k
 // y = A x with A the plan's block lower-triangular Toeplitz system matrix (the matrix
 // ft_solve_fast inverts): far history through the schedule's own FFT / direct products
 // (O(M N log N)), in-leaf lags and the spatial stencil by apply_near_kernel.
+static int apply_launches(ft_plan* p, const double* x, double* y, cudaStream_t st);
 static int apply_impl(ft_plan* p, const double* x, double* y) {
     if (!p || !x || !y) return set_err(FT_EINVAL, "ft_apply: bad argument");
     if (p->stencil) return set_err(FT_EINVAL, "ft_apply: Scheme 2 (stencil history) plans are not supported");
@@ -1722,7 +1726,36 @@ static int apply_impl(ft_plan* p, const double* x, double* y) {
     if (!is_device_ptr(x) || !is_device_ptr(y) || x == y)
         return set_err(FT_EINVAL, "ft_apply: x and y must be distinct buffers, both on the device or both on the host");
     FT_CUDA(cudaSetDevice(p->device));
-    cudaStream_t st = p->stream;
+    // the launch sequence (up to ~2 N / L products) replays as one CUDA graph per buffer pair: a
+    // Krylov caller applies the operator hundreds of times to the same device vectors
+    if (!getenv("FT_NO_GRAPH")) {
+        if (p->apply_graph && p->apply_x == x && p->apply_y == y) {
+            FT_CUDA(cudaGraphLaunch(p->apply_graph, p->stream));
+            return FT_OK;
+        }
+        if (p->apply_graph) cudaGraphExecDestroy(p->apply_graph);
+        p->apply_graph = nullptr;
+        cudaStream_t cs;
+        FT_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        FT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        const int rc = apply_launches(p, x, y, cs);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        FT_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&p->apply_graph, g, 0);
+        cudaGraphDestroy(g);
+        FT_CUDA(ie);
+        p->apply_x = x;
+        p->apply_y = y;
+        FT_CUDA(cudaGraphLaunch(p->apply_graph, p->stream));
+        return FT_OK;
+    }
+    return apply_launches(p, x, y, p->stream);
+}
+
+static int apply_launches(ft_plan* p, const double* x, double* y, cudaStream_t st) {
     const uint64_t N = p->N;
     FT_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * rows_of(p) * N, st));
     for (const Op& op : p->ops) {
@@ -1770,7 +1803,8 @@ int ft_apply(ft_plan* p, const double* x, double* y) {
             return set_err(FT_ENOMEM, "ft_apply: device staging buffers");
         }
         cudaError_t e = cudaMemcpyAsync(xd, x, bytes, cudaMemcpyHostToDevice, p->stream);
-        int rc = e == cudaSuccess ? apply_impl(p, xd, yd) : set_err(FT_ECUDA, cudaGetErrorString(e));
+        // (temporary buffers: launched directly, not through the cached graph)
+        int rc = e == cudaSuccess ? apply_launches(p, xd, yd, p->stream) : set_err(FT_ECUDA, cudaGetErrorString(e));
         if (!rc) {
             e = cudaMemcpyAsync(y, yd, bytes, cudaMemcpyDeviceToHost, p->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
@@ -1906,6 +1940,7 @@ void ft_destroy(ft_plan* p) {
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->apply_graph) cudaGraphExecDestroy(p->apply_graph);
     if (p->nccl_comm) nccl_api().CommDestroy(p->nccl_comm);
     if (p->rdev_d) cudaFree(p->rdev_d);
     for (void* q : p->p2p_opened) cudaIpcCloseMemHandle(q);
