@@ -116,15 +116,23 @@ typedef struct ft_options {
     int near_field;        /* lags < near_field are summed exactly in every history
                               product (0 = default: 1 for ODE/diffusion, 64 for wave) */
     int device;            /* CUDA device ordinal (-1 = current) */
-    int reserved;
+    int flags;             /* FT_OPT_* bits (0 = defaults) */
 } ft_options;
+
+enum {
+    FT_OPT_REPORT_RESIDUAL = 1  /* ft_solve_fast / ft_solve_direct on device buffers (rhs != u) fill
+                                   ft_report::residual with max |A u - rhs| / max |rhs|, measured by one
+                                   application of the plan's operator (ft_residual); off by default
+                                   because it costs about as much as the solve's history products */
+};
 
 typedef struct ft_report {
     char method[16];       /* "fast" / "direct" (SolveReport::method) */
     uint64_t iterations;   /* 0: both paths are direct methods (no Krylov matvecs) */
-    double residual;       /* always 0: both paths are direct solves (no iteration, no residual
+    double residual;       /* 0 by default: both paths are direct solves (no iteration, no residual
                               estimate), as the reference's Direct path reports 0 (SolveReport
-                              defaults, schemes.hpp:58-63); parity is checked against the oracle */
+                              defaults, schemes.hpp:58-63); with FT_OPT_REPORT_RESIDUAL the measured
+                              max |A u - rhs| / max |rhs| (the reference's GMRES reports ||r||_2 / ||b||_2) */
     double seconds;        /* wall time of the call (SolveReport::seconds) */
     double device_ms;      /* device time of the solve proper (CUDA events) */
     uint64_t kernel_launches;  /* kernels this library launched for the call */

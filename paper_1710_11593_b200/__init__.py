@@ -66,7 +66,7 @@ class _Problem(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("rhs_mode", C.c_int), ("near_field", C.c_int), ("device", C.c_int),
-                ("reserved", C.c_int)]
+                ("flags", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -246,7 +246,7 @@ class Plan:
     ft_setup_toeplitz)."""
 
     def __init__(self, problems, rhs_mode: int = FT_RHS_REFERENCE, near_field: int = 0,
-                 device: int = -1, partition=None, _handle=None):
+                 device: int = -1, partition=None, _handle=None, report_residual: bool = False):
         if _handle is not None:
             self.specs = []
             h = _handle
@@ -255,7 +255,7 @@ class Plan:
                 problems = [problems]
             self.specs = list(problems)
             arr = (_Problem * len(self.specs))(*[p._c() for p in self.specs])
-            opt = _Options(rhs_mode, near_field, device, 0)
+            opt = _Options(rhs_mode, near_field, device, 1 if report_residual else 0)
             h = C.c_void_p()
             if partition is None:
                 _check(lib().ft_setup_batch(arr, len(self.specs), C.byref(opt), C.byref(h)))

@@ -142,6 +142,7 @@ struct ft_plan {
     double* wts_d = nullptr;
     double* lampow_d = nullptr;
     int lp_stride = 0;
+    bool report_residual = false;  // FT_OPT_REPORT_RESIDUAL
     bool paired_g = false;       // resp_g holds the mirror-pair tables (phase 3 of the slab leaf)
     cplx* tw_d = nullptr;
     cplx* spec_d = nullptr;
@@ -452,6 +453,7 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
     p->tau = z.time_length / (double)z.time_steps;
     p->h = z.scheme == FT_SCHEME_ODE ? 0.0 : z.space_length / (double)z.space_cells;
     p->rhs_mode = opt ? opt->rhs_mode : 0;
+    p->report_residual = opt && (opt->flags & FT_OPT_REPORT_RESIDUAL);
     p->J = (opt && opt->near_field > 0) ? opt->near_field : (z.scheme == FT_SCHEME_WAVE ? 64 : 1);
     if (opt && opt->device >= 0) FT_CUDA(cudaSetDevice(opt->device));
     FT_CUDA(cudaGetDevice(&p->device));
@@ -1538,6 +1540,14 @@ static int solve_common(ft_plan* p, const double* rhs, double* u, ft_report* rep
         rep->residual = 0.0;
         rep->device_ms = ms;
         rep->kernel_launches = launches;
+        // FT_OPT_REPORT_RESIDUAL: measure max |A u - rhs| / max |rhs| through the plan's operator
+        // (device buffers, rhs kept: one operator application, about the cost of the solve's products)
+        if (p->report_residual && rhs_dev && u_dev && rhs != u && !p->stencil && p->part_world == 1) {
+            double r = 0.0, m = 0.0;
+            const int rc = ft_residual(p, rhs, u, nullptr, &r, &m);
+            if (rc) return rc;
+            rep->residual = m > 0.0 ? r / m : r;
+        }
         rep->seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     }

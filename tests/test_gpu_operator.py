@@ -193,3 +193,22 @@ def test_operator_entries_equal_time_marching_matrix(ft, scheme, cells, steps):
     assert np.array_equal(got[off], A[off])
     d = np.abs(np.diag(got) - np.diag(A)) / np.abs(np.diag(A))
     assert d.max() <= 2.3e-16
+
+
+def test_report_residual_option(ft):
+    """ft_report::residual: 0 by default (direct method, as the reference's Direct path), the measured
+    max |A u - rhs| / max |rhs| with FT_OPT_REPORT_RESIDUAL (SolveReport::residual, schemes.hpp:58-63)."""
+    import torch
+
+    w = W.config(2, time_steps=2048)
+    plain = ft.Plan(w.specs)
+    R = torch.empty(plain.shape, dtype=torch.float64, device="cuda")
+    plain.assemble_rhs_modes(R, w.a, w.k, w.p, w.trig, w.u0amp, w.phiamp)
+    _, rep0 = plain.solve_fast(R)
+    assert rep0.residual == 0.0
+    plan = ft.Plan(w.specs, report_residual=True)
+    Uf, repf = plan.solve_fast(R)
+    Ud, repd = plan.solve_direct(R)
+    res, rmax = plan.residual(R, Uf)
+    assert 0.0 < repf.residual <= 1e-10 and repf.residual == res / rmax
+    assert 0.0 < repd.residual <= 1e-10
