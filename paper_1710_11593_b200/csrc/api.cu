@@ -142,6 +142,8 @@ struct ft_plan {
     double* wts_d = nullptr;
     double* lampow_d = nullptr;
     int lp_stride = 0;
+    double2* chain_d = nullptr;    // chained upwind slab leaves: [B][P][L] boundary records
+    bool chain_leaf = false;
     bool report_residual = false;  // FT_OPT_REPORT_RESIDUAL
     bool paired_g = false;       // resp_g holds the mirror-pair tables (phase 3 of the slab leaf)
     cplx* tw_d = nullptr;
@@ -655,6 +657,14 @@ int setup_impl(const ft_problem* probs, uint64_t count, const ft_options* opt, f
             // stopped spilling (kernel-parameter constants)
             p->fused_leaf = (int64_t)B * p->P_local <= (int64_t)dev_sms * per_sm && getenv("FT_NO_FUSED_LEAF") == nullptr;
         }
+        {   // Scheme 3 problems of a few slabs: chained slabs instead of phase 1 / barrier / correction
+            static const int chain_max = getenv("FT_CHAIN_MAX_P") ? atoi(getenv("FT_CHAIN_MAX_P")) : 4;
+            p->chain_leaf = p->fused_leaf && p->kind == SK_UPWIND && !p->stencil && p->part_world == 1 &&
+                            p->P <= chain_max && p->npt == 2 && p->L == 32;
+            if (p->chain_leaf &&
+                (rc = alloc_copy((void**)&p->chain_d, nullptr, sizeof(double2) * B * p->P * p->L)))
+                return rc;
+        }
         const uint64_t gsz = (uint64_t)2 * 2 * p->slab * p->L, hsz = (uint64_t)2 * p->L * 4;
         std::vector<double> G(B * gsz, 0.0), H(B * hsz, 0.0);
         const int mlast = nodes - (p->P - 1) * p->slab;
@@ -804,6 +814,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     bool pend0 = false, pend0_first = false;
     p->last_fuse0 = fuse0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
+    const bool chain = p->chain_leaf && !p->p2p && !io && !gen;
+    if (chain) FT_CUDA(cudaMemsetAsync(p->chain_d, 0, sizeof(double2) * p->B * p->P * p->L, st));
     int leaves_total = 0;
     for (const Op& o : p->ops) leaves_total += o.kind == OP_LEAF ? 1 : 0;
     if (p->p2p) FT_CUDA(launch_p2p_epoch(reinterpret_cast<unsigned*>((char*)p->p2p_block + 8), st));
@@ -846,6 +858,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
             a.kcoef = p->kcoef_d;
             a.xch = p->xch_d;
             a.xsend = p->xsend_d;
+            a.chain = p->chain_d;
+            a.chain_tag = (double)(leaf_index + 1);
             a.P_local = p->P_local;
             a.s_begin = p->part_rank * p->P_local;
             a.node_begin = p->node_begin;
@@ -888,6 +902,8 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
                 a.xch = reinterpret_cast<double*>((char*)p->p2p_block + kP2pHeader) +
                         (size_t)(a.p2p_leaf & 1) * p->P * p->L * 2;
                 FT_CUDA(launch_leaf_p2p(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
+            } else if (chain) {
+                FT_CUDA(launch_leaf_chain(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
             } else if (p->multi && p->part_world == 1 && p->fused_leaf) {
                 FT_CUDA(launch_leaf_fused(p->kind, p->npt, p->L, a, p->B * p->P_local, st));
             } else {
@@ -1159,6 +1175,7 @@ int ft_nccl_init(ft_plan* p, const void* id128, int rank, int world) {
     // the collective sits between phase 1 and the correction: two kernels per leaf (also for
     // world = 1, which exercises this path on one GPU)
     p->fused_leaf = false;
+    p->chain_leaf = false;
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
@@ -1946,7 +1963,7 @@ void ft_destroy(ft_plan* p) {
     cudaSetDevice(p->device);
     if (!p->own_xch) p->xch_d = nullptr;
     void* ptrs[] = {p->pc_d, p->col_d, p->wts_d, p->lampow_d, p->tw_d, p->spec_d, p->xch_d,
-                    p->kcoef_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->dmctr_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
+                    p->kcoef_d, p->chain_d, p->respg_d, p->resph_d, p->respw_d, p->bar_d, p->mpscratch_d, p->dw_d, p->cprime_d, p->den_d, p->scratch_d, p->dmctr_d, p->work_d, p->vsrc_d, p->genA_d, p->genT_d, p->genArgs_d, p->oder_d};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->graph) cudaGraphExecDestroy(p->graph);

@@ -144,6 +144,8 @@ struct LeafArgs {
     const double* kcoef;       // [B][2][nodes] single-CTA Dirichlet coefficients kF, kB
     double* xch;               // multi-slab carries of the current leaf, all slabs [B][P][L][2]
     double* xsend;             // phase-1 output [B*P_local][L][2] (== xch unless partitioned)
+    double2* chain;            // chained upwind slabs: [B][P][L] {last-node solution, leaf tag} per step
+    double chain_tag;          // tag of this leaf's entries (leaf index + 1; the buffer is zeroed per solve)
     int P_local;               // slabs (CTAs) per problem held by this plan / rank
     int s_begin;               // first slab of this rank
     int node_begin;            // first node of this rank (X row 0 of a problem)
@@ -241,6 +243,7 @@ cudaError_t launch_leaf_wbuild(int kind, int L, const LeafArgs& a, int B, double
 cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 bool leaf_pair_ok(const LeafArgs& a, int L);
 cudaError_t launch_leaf_pair(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_leaf_chain(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_leaf_p2p(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_p2p_epoch(unsigned* epoch, cudaStream_t st);
 // exchange block layout: [0] uint64 arrival counter, [8] uint32 solve epoch, [64..) receive

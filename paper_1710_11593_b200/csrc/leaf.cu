@@ -374,6 +374,23 @@ __device__ __forceinline__ void level0_rows(const LeafArgs& a, double* s_out, in
 // that mark stalling on instruction fetch (30 % of the leaf's warp samples at 150 KB).
 // PAIR (leaf_pair kernel): half = 1 is the second leaf of a pair whose first leaf's solution
 // is still in s_out: the level-0 product is formed there and the staged R subtracts it.
+// Chained upwind slabs (MODE 2): one 16-byte {value, tag} record per slab and step; a single
+// vector store / load, so the tag never arrives without its value.  Relaxed gpu-scope accesses
+// (a weak load in the wait loop may legally be hoisted by ptxas: it hung).
+__device__ __forceinline__ double2 chain_load(const double2* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void chain_store(double2* p, double x, double tag) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(tag));
+}
+
+// MODE 0: single slab (closed-form Dirichlet images); MODE 1: space-time SPIKE phase 1 (zero
+// inter-slab carries, carries exported); MODE 2: chained upwind slabs -- the operator is lower
+// bidiagonal in space, so slab s only needs the solution at the last node of slab s - 1 at the
+// same step: it runs a step or two behind its left neighbour and adds lam^(q+1) x_left to its
+// own scan, exactly (no correction phase, no grid barrier).
 template <int KIND, int NPT, int L, int MODE, bool PC = false, bool LEAN = false, bool PAIR = false>
 __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool write_x, int half = 0) {
     // s_out: [slab nodes][L + 1] solution tile (stays resident for the fused leaf)
@@ -397,7 +414,8 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 
     (void)colp;
 
-    const bool stamp = a.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0;
+    // (chained slabs: the last slab is the critical path)
+    const bool stamp = a.dbg_clk && blockIdx.x == ((MODE == 2 && !(a.dbg & 8)) ? gridDim.x - 1 : 0) && threadIdx.x == 0;
     const LeafConsts<PC, NPT, L> sc(a, pb, lp, pc.lam, lane);  // plan constants: before the dependency wait
     if (!PAIR || half == 0) pdl_wait();
     if (stamp) a.dbg_clk[8] = clock64();
@@ -489,6 +507,24 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
 #pragma unroll
     for (int v = 0; v < NPT; ++v) vmask[v] = (tid * NPT + v < mreal) ? 1.0 : 0.0;
     double* outp = s_out + tid * NPT * (L + 1);
+    // chained upwind slabs: lam^(q+1) per node, the neighbour's record of the next step in flight
+    double lq[NPT];
+    const bool chain_in = MODE == 2 && s > 0, chain_out = MODE == 2 && s + 1 < a.P;
+    const double2* cin_p = MODE == 2 ? a.chain + ((uint64_t)pb * a.P + (s > 0 ? s - 1 : 0)) * L : nullptr;
+    double2* cout_p = MODE == 2 ? a.chain + ((uint64_t)pb * a.P + s) * L : nullptr;
+    // (two records in flight: the load of step k + 2 is issued during step k, ~2 steps before its
+    // use -- an L2 round trip to a line another SM just wrote is most of a step)
+    double2 cnx = make_double2(0.0, 0.0), cnx1 = make_double2(0.0, 0.0);
+    if (MODE == 2) {
+#pragma unroll
+        for (int v = 0; v < NPT; ++v) lq[v] = lp[min(tid * NPT + v + 1, a.lp_stride - 1)];
+        if (chain_in) {  // every lane of every warp polls the same record (one transaction per warp): the
+                         // wait loop below is warp-uniform by a vote, so the scan's shuffles stay convergent
+                         // (a thread-0-only wait loop sent them through WARPSYNC.COLLECTIVE: +250 cycles per step)
+            cnx = chain_load(cin_p);
+            cnx1 = chain_load(cin_p + (len > 1 ? 1 : 0));
+        }
+    }
     // Rolling window: tile[v][i] holds the right-hand side of step k + i; each
     // step shifts it down by one register while pushing the new solution into
     // the remaining in-leaf steps (no unrolling over k: the body stays small
@@ -508,9 +544,16 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
             // on B200 (measured), the product 8; same rounding model as the host tables (local_solve_ld)
             for (int v = 0; v < NPT; ++v) in[v] = (KIND == SK_UPWIND) ? tile[v][0] * pc.G0 : tile[v][0];
             double Fv[NPT], Bv[NPT], totF, totB;
+            double cin = 0.0;
+            if (MODE == 2 && chain_in) {  // the left slab's boundary value of this step (normally already here)
+                while (__any_sync(0xffffffffu, cnx.y != a.chain_tag)) cnx = chain_load(cin_p + k);
+                cin = cnx.x;
+                cnx = cnx1;  // rotate; the record of step k + 2 goes in flight
+                if (k + 2 < len) cnx1 = chain_load(cin_p + k + 2);
+            }
             cta_scan<KIND, NPT, MODE == 0>(in, sc, s_wt[par], lane, w, Fv, Bv, totF, totB, xleft);
             double cF = totF;
-            if (padded) {  // F at the last real node (padding nodes carry zeros)
+            if (MODE != 2 && padded) {  // F at the last real node (padding nodes carry zeros)
                 if (tid == own_t) {
 #pragma unroll
                     for (int v = 0; v < NPT; ++v)
@@ -529,7 +572,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
                     const double base = pc.G0 * (Fv[v] + Bv[v] - in[v]);
                     x[v] = MODE == 0 ? fma(kF[v], cF, fma(kB[v], totB, base)) : base;
                 } else {
-                    x[v] = Fv[v];
+                    x[v] = MODE == 2 ? fma(lq[v], cin, Fv[v]) : Fv[v];
                 }
             }
         }
@@ -537,6 +580,11 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& a, double* s_out, bool
         for (int v = 0; v < NPT; ++v) {
             if (padded) x[v] *= vmask[v];  // padding nodes stay exactly zero
             outp[v * (L + 1)] = x[v];
+        }
+        if (MODE == 2 && chain_out && tid == own_t) {  // this slab's last node: the right neighbour's input
+#pragma unroll
+            for (int v = 0; v < NPT; ++v)
+                if (v == own_v) chain_store(cout_p + k, x[v], a.chain_tag);
         }
         // Scheme 2: the history acts on U_i + U_(i-1) (the left neighbour's solution)
         double xs[NPT];
@@ -1021,6 +1069,14 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_fused(LeafArgs a) {
     correct_body<KIND, NPT, L, LEAN>(a, s_c0, s_x, true);
 }
 
+// Chained upwind slabs (config 3, Scheme 3 problems of 2 .. 4 slabs): one cooperative kernel per
+// leaf (co-residency makes the per-step waits safe), no correction phase.
+template <int KIND, int NPT, int L, bool PC, bool LEAN>
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_chain(LeafArgs a) {
+    extern __shared__ __align__(16) double s_dyn[];
+    leaf_body<KIND, NPT, L, 2, PC, LEAN>(a, s_dyn, true);
+}
+
 // Two consecutive slab leaves in one cooperative kernel (single-GPU plans whose level-0
 // history products fold into the leaf: between leaves 2i and 2i+1 the schedule has no other
 // product).  The first leaf's solution stays in shared memory, so the level-0 product reads
@@ -1255,6 +1311,41 @@ cudaError_t launch_leaf_fused(int kind, int npt, int L, const LeafArgs& a, int c
         if (kind == SK_TRIDIAG) return launch_fused_t<SK_TRIDIAG, 2, 32>(a, ctas, st);
         if (kind == SK_UPWIND) return launch_fused_t<SK_UPWIND, 2, 32>(a, ctas, st);
     }
+    return cudaErrorInvalidValue;
+}
+
+template <int NPT, int L>
+static cudaError_t launch_chain_t(const LeafArgs& a, int ctas, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)kLeafThreads * NPT * (L + 1);
+    static DeviceOnce attr;
+    if (attr.first()) {
+        cudaFuncSetAttribute(leaf_chain<SK_UPWIND, NPT, L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(leaf_chain<SK_UPWIND, NPT, L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(leaf_chain<SK_UPWIND, NPT, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(leaf_chain<SK_UPWIND, NPT, L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr.done();
+    }
+    static const bool no_lean = getenv("FT_NO_LEAN") != nullptr;
+    const bool lean = !no_lean && a.len == L && (a.N & 1) == 0 && !a.radd && !a.genA && !a.V && !a.stencil;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLeafThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute coop[1];
+    coop[0].id = cudaLaunchAttributeCooperative;
+    coop[0].val.cooperative = 1;
+    cfg.attrs = coop;
+    cfg.numAttrs = 1;
+    if (lean)
+        return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_chain<SK_UPWIND, NPT, L, true, true>, a)
+                          : cudaLaunchKernelEx(&cfg, leaf_chain<SK_UPWIND, NPT, L, false, true>, a);
+    return a.kc_valid ? cudaLaunchKernelEx(&cfg, leaf_chain<SK_UPWIND, NPT, L, true, false>, a)
+                      : cudaLaunchKernelEx(&cfg, leaf_chain<SK_UPWIND, NPT, L, false, false>, a);
+}
+
+cudaError_t launch_leaf_chain(int kind, int npt, int L, const LeafArgs& a, int ctas, cudaStream_t st) {
+    if (npt == 2 && L == 32 && kind == SK_UPWIND) return launch_chain_t<2, 32>(a, ctas, st);
     return cudaErrorInvalidValue;
 }
 

@@ -29,7 +29,14 @@ def test_native_nccl_exchange_one_rank(ft, cid, kw):
     plan2.nccl_init(uid, 0, 1)
     U1, rep1 = plan2.solve_fast(R)
     U2, rep2 = plan2.solve_fast(R)   # graph replay with the collectives inside
-    assert torch.equal(U1, U0) and torch.equal(U2, U0)
+    assert torch.equal(U2, U1)
+    if cid == 3:
+        # Scheme 3 plans of <= 4 slabs default to the chained-slab leaf (exact, no correction phase):
+        # same solution as the phase-1 / all-gather / correction path to rounding, not to the bit
+        err = ((U1 - U0).abs().max() / U0.abs().max()).item()
+        assert err <= 1e-12, err
+    else:
+        assert torch.equal(U1, U0)
     leaves = (plan.N + 31) // 32
     # two kernels per leaf (the collective between them) instead of one cooperative kernel
     assert rep1.kernel_launches >= 2 * leaves and rep1.kernel_launches == rep2.kernel_launches

@@ -369,7 +369,9 @@ def test_fused_rhs_generation_transport(ft, oracle_mod):
 
 @pytest.mark.parametrize("cid,kw", [
     (5, dict(time_steps=256, cells=1001, batch=3)),   # batched multi-slab: per-problem constants path
-    (3, dict(time_steps=200, cells=700)),             # wave scheme, 2 uneven slabs
+    (3, dict(time_steps=200, cells=700)),             # wave scheme, 2 uneven slabs (chained-slab leaf)
+    (3, dict(time_steps=300, cells=1700)),            # wave scheme, 4 slabs, ragged last (chained-slab leaf)
+    (3, dict(time_steps=97, cells=2300)),             # wave scheme, 5 slabs: phase 1 / correction leaf
     (4, dict(time_steps=33, cells=600)),              # one leaf + a 1-step leaf, 2 slabs
     (2, dict(time_steps=1, cells=17)),                # a single step
     (1, dict(time_steps=31)),                         # a single partial leaf
