@@ -814,7 +814,7 @@ int run_fast(ft_plan* p, double* X, const double* rhs, uint64_t* launches,
     bool pend0 = false, pend0_first = false;
     p->last_fuse0 = fuse0;
     if (p->multi && p->part_world == 1 && p->fused_leaf) FT_CUDA(cudaMemsetAsync(p->bar_d, 0, sizeof(unsigned), st));
-    const bool chain = p->chain_leaf && !p->p2p && !io && !gen;
+    const bool chain = p->chain_leaf && !p->p2p;
     if (chain) FT_CUDA(cudaMemsetAsync(p->chain_d, 0, sizeof(double2) * p->B * p->P * p->L, st));
     int leaves_total = 0;
     for (const Op& o : p->ops) leaves_total += o.kind == OP_LEAF ? 1 : 0;

@@ -34,6 +34,6 @@ cap mp1g12 "mp1g_kernel<.int.12>" 4
 cap direct64 "mp_direct_kernel" 300
 cap ode_whole "ode_whole_kernel" 0 --config 1
 cap leaf_cfg2 "leaf_kernel" 60 --config 2
-cap leaf_cfg3 "leaf_fused" 60 --config 3 --time-steps 8192
+cap leaf_cfg3 "leaf_chain" 60 --config 3 --time-steps 8192
 cp /tmp/ncu/cap_leaf_pair.ncu-rep /tmp/ncu/cap_split16.ncu-rep $O/ 2>/dev/null
 du -sh $O

@@ -15,6 +15,7 @@ KERNELS = {
     "mp_split_kernel_8": r"_ZN3ftb15mp_split_kernelILi8ELi12EEEvNS_6MpArgsENS_6SplitQE",
     "leaf_pair_tridiag": r"_ZN3ftb9leaf_pairILi2ELi2ELi32EEEvNS_8LeafArgsE",
     "leaf_fused_tridiag": r"_ZN3ftb10leaf_fusedILi2ELi2ELi32ELb1ELb1EEEvNS_8LeafArgsE",
+    "leaf_chain_upwind": r"_ZN3ftb10leaf_chainILi1ELi2ELi32ELb1ELb1EEEvNS_8LeafArgsE",
     "mp1g_kernel_9": r"_ZN3ftb11mp1g_kernelILi9EEEvNS_6MpArgsE",
     "mp1p_kernel_12_tma": r"_ZN3ftb11mp1p_kernelILi12EEEvNS_6MpArgsEi",
     "mp8_kernel_9_radix8": r"_ZN3ftb10mp8_kernelILi9EEEvNS_6MpArgsE",
